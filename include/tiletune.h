@@ -1,0 +1,266 @@
+/*
+ * tiletune.h -- C-ABI of libtiletune, the B200 (sm_100a) hot path of arXiv 1909.10616
+ * "Compiler-Level Matrix Multiplication Optimization for Deep Learning" (G-BFS / N-A2C).
+ *
+ * Citations: P:n = line n of the paper's PAPER.md; S:n = line n of SPEC.md; readings Z1..Z23
+ * and the J_hw table are in DESIGN.md.
+ *
+ * Conventions (apply to every entry point):
+ *  - Every function returns tt_status and never throws across the ABI.  On a non-OK status a
+ *    thread-local message is available from tt_last_error().
+ *  - Argument order: the ABI takes (M, N, K) for C[M x N] = A[M x K] . B[K x N].  The paper
+ *    names problems (m, k, n) and orders the state [s_m, s_k, s_n];
+ *    tt_config keeps that paper order (m, k, n).  M == m, N == n, K == k.
+ *  - Matrices are dense row-major: A[M][K], B[K][N], C[M][N] (reading Z14); C is overwritten.
+ *  - Ownership: the caller owns every buffer passed in (host arrays and device A/B/C).  The
+ *    library keeps no pointer past return.  Only a tt_ctx owns device memory (measurement
+ *    operands, events, an L2-flush buffer, host staging for tt_gemm_host).
+ *  - Threading: the configuration-space functions (tt_count_configs .. tt_neighbors,
+ *    tt_binding) are pure and thread-safe.  A tt_ctx is used by one thread at a time;
+ *    measurement is serialised per device.
+ */
+#ifndef TILETUNE_H
+#define TILETUNE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TT_VERSION 1
+#define TT_MAXD 4  /* maximum loop depth per axis carried in tt_config */
+
+typedef enum {
+  TT_OK = 0,
+  TT_E_INVAL = 1,          /* bad argument (null pointer, size, depth > TT_MAXD, illegitimate s0) */
+  TT_E_ILLEGITIMATE = 2,   /* J_prod false: Eq. 2-4 products or positivity violated */
+  TT_E_INFEASIBLE = 3,     /* J_hw false for the requested family */
+  TT_E_OVERFLOW = 4,       /* space size does not fit uint64 */
+  TT_E_CAPACITY = 5,       /* output buffer too small; *n_out holds the size needed */
+  TT_E_CUDA = 6,           /* CUDA runtime / driver error (message in tt_last_error) */
+  TT_E_EVALUATOR = 7,      /* cost source failed during a search; partial result + trace valid */
+  TT_E_UNSUPPORTED = 8     /* family / depth combination has no kernel */
+} tt_status;
+
+/* Kernel families = J_hw tables. */
+typedef enum {
+  TT_FAM_NONE = 0,         /* J = J_prod only (the paper's space); no kernel */
+  TT_FAM_F32_SIMT = 1,     /* K1: fp32 CUDA-core FFMA, the paper's arithmetic (reading Z13) */
+  TT_FAM_TF32_UMMA = 2,    /* K2: tcgen05.mma kind::tf32, fp32 storage, fp32 accumulate */
+  TT_FAM_BF16_UMMA = 3     /* K3: tcgen05.mma kind::f16 with bf16 A/B, fp32 accumulate */
+} tt_family;
+
+/* Problem instance: the paper's cost(s; m,k,n,d_m,d_k,d_n), plus the J_hw family. */
+typedef struct {
+  int64_t M, N, K;         /* C[M x N] = A[M x K] B[K x N]; all >= 1 */
+  int32_t dm, dk, dn;      /* loop depths d_m, d_k, d_n, 1..TT_MAXD; paper uses 4,2,4 */
+  int32_t family;          /* tt_family */
+} tt_space;
+
+/* A state s = [s_m, s_k, s_n] (Eq. 5).  Factor vectors outer -> inner (reading Z1):
+ * m[i] = trip count of the i-th m loop.  Slots >= d_x must be 1. */
+typedef struct {
+  int64_t m[TT_MAXD], k[TT_MAXD], n[TT_MAXD];
+} tt_config;
+
+/* Result of one measurement ("arithmetic mean for 10 repeated trials"; reading Z10). */
+typedef struct {
+  double cost_s;           /* median of per-repeat means (the score the searches use) */
+  double mean_s, min_s, stdev_s;
+  double probe_s;          /* one timed launch before the repeats */
+  int32_t repeats;         /* R actually run (1 when the slow-candidate cut fired, Z12) */
+  int32_t number;          /* back-to-back launches per repeat */
+  int32_t device;          /* CUDA ordinal the sample was taken on */
+  int32_t slow_cut;        /* 1 if cost_s = probe_s because probe_s > cut_s (Z12) */
+} tt_sample;
+
+typedef struct {
+  int32_t warmup;          /* untimed launches before the probe (default 2) */
+  int32_t repeats;         /* R (default 10) */
+  double min_repeat_s;     /* each repeat lasts >= this: number = ceil(min_repeat_s / probe) (5e-4) */
+  double cut_s;            /* if > 0 and probe > cut_s: cost = probe, repeats = 1 (Z12) */
+  int32_t l2_flush;        /* 1: overwrite a >= 2 x L2 buffer before every timed launch */
+  int32_t max_number;      /* cap on `number` (default 1000) */
+} tt_measure_opts;
+
+/* One row per measured state, in evaluation order (Fig. 7 axes P:352). */
+typedef struct {
+  uint64_t eval_index;     /* 0 = s0 */
+  double t_wall_s;         /* host wall clock since the search started */
+  tt_config cfg;
+  double cost_s;
+  double best_so_far_s;
+} tt_trace_row;
+
+typedef struct {
+  tt_config best;          /* s* (Alg. 1 line 16 / Alg. 2 line 26) */
+  double best_cost_s;      /* cost_min */
+  uint64_t evals;          /* distinct states measured, s0 included (reading Z19) */
+  uint64_t space_raw;      /* card(xi), the paper's denominator */
+  uint64_t space_feasible; /* states with J_prod and J_hw */
+  double frac_raw;         /* evals / space_raw ("fraction of visited configurations") */
+  double frac_feasible;    /* evals / space_feasible */
+  double wall_s;           /* tuning wall time ("searching time") */
+  uint64_t trace_len;      /* rows written to the trace buffer (<= trace_cap) */
+} tt_result;
+
+/* Cost sources (how a search scores candidates). */
+typedef enum {
+  TT_COST_DEVICE = 0,      /* tt_measure on the ctx's device (the hardware test of P:231) */
+  TT_COST_CALLBACK = 1,    /* cost_fn(cfg, user) per state (synthetic landscapes) */
+  TT_COST_TABLE = 2,       /* table[rank(cfg)] (deterministic tables / trace replay) */
+  TT_COST_BATCH = 3        /* batch_fn(cfgs, n, costs, user) per round (multi-GPU sharding) */
+} tt_cost_source;
+
+typedef double (*tt_cost_fn)(const tt_config* cfg, void* user);
+/* Must fill costs[0..n) and return 0; nonzero aborts the search with TT_E_EVALUATOR. */
+typedef int32_t (*tt_batch_eval_fn)(const tt_config* cfgs, int32_t n, double* costs, void* user);
+
+typedef struct {
+  int32_t family;          /* tt_family of the searched space */
+  int32_t dm, dk, dn;      /* loop depths (default 4,2,4) */
+  uint64_t seed;           /* SplitMix64 seed (reading O7) */
+  int32_t has_s0;          /* 1: start from s0 below; 0: per-family default (P:369 / Z3) */
+  tt_config s0;
+  double budget_seconds;   /* T_max; <= 0: none */
+  int32_t cost_source;     /* tt_cost_source */
+  tt_cost_fn cost_fn;
+  tt_batch_eval_fn batch_fn;
+  void* user;
+  const double* table;     /* TABLE source: cost by rank, length table_len (= space_raw) */
+  uint64_t table_len;
+  tt_measure_opts measure; /* DEVICE source */
+  /* G-BFS (Alg. 1) */
+  int32_t rho;             /* neighbours sampled per expansion (default 5) */
+  int32_t width;           /* states popped per round W (default 1 = Alg. 1; Z9) */
+  /* N-A2C (Alg. 2; defaults per reading Z18 / S:417-423) */
+  int32_t steps_T;         /* exploration steps T (default 3) */
+  double epsilon;          /* exploitation probability (default 0.8) */
+  int32_t batch;           /* len(B_test) (default 16) */
+  int32_t mem_capacity;    /* |M| FIFO capacity (default 4096) */
+  double gamma, beta, lr, clip;   /* 0.9, 0.01, 0.01, 1.0 */
+  int32_t epochs, minibatch, hidden;   /* 4, 64, 64 */
+  int32_t rollout_cap_factor, max_t_increase;   /* 50, 16 */
+} tt_search_opts;
+
+/* How a config is bound to a launch (a5 of SURVEY §8a; for tests and reports). */
+typedef struct {
+  int32_t family;
+  int64_t grid_x, grid_y, grid_z;
+  int32_t block_x;
+  int32_t cluster_x;
+  int32_t smem_bytes;      /* dynamic shared memory */
+  int32_t stages;          /* pipeline depth */
+  int32_t tile_m, tile_n, tile_k;   /* per-cluster output tile and K step */
+  int32_t tmem_cols;       /* UMMA: allocated TMEM columns (0 for SIMT) */
+  int32_t acc_buffers;     /* UMMA: TMEM accumulator buffers */
+  uint32_t idesc;          /* UMMA: instruction descriptor */
+  int32_t reg_tile_m, reg_tile_n;   /* SIMT: per-thread register tile m3 x n3 */
+} tt_launch_info;
+
+typedef struct tt_ctx tt_ctx;
+
+int32_t tt_version(void);
+const char* tt_last_error(void);
+void tt_search_opts_default(tt_search_opts* opts);
+void tt_measure_opts_default(tt_measure_opts* opts);
+
+/* ---------------------------------------------------------------- configuration space (host) */
+
+/* card(xi) = prod_x prod_{p^e || x} C(e + d_x - 1, d_x - 1) (Eq. 1-4; P:375 prints
+ * 899756 for 1024^3).  *feasible (nullable) counts states with J_hw too (enumerates the raw
+ * space: milliseconds up to ~3M states).  TT_E_OVERFLOW if raw does not fit uint64. */
+tt_status tt_count_configs(const tt_space* sp, uint64_t* raw, uint64_t* feasible);
+
+/* States with J_prod true, in rank order (lexicographic over m0.., k0.., n0..; reading O4),
+ * ranks [first_rank, first_rank + cap).  *n_out = number written. */
+tt_status tt_enumerate_configs(const tt_space* sp, uint64_t first_rank, uint64_t cap,
+                               tt_config* out, uint64_t* n_out);
+
+/* Every state with J = J_prod and J_hw, in rank order.  cfgs and/or ranks may be null (count
+ * only).  TT_E_CAPACITY with *n_out = needed if cap is too small. */
+tt_status tt_enumerate_feasible(const tt_space* sp, uint64_t cap, tt_config* cfgs,
+                                uint64_t* ranks, uint64_t* n_out);
+
+/* rank = (r_m |xi_k| + r_k) |xi_n| + r_n.  TT_E_ILLEGITIMATE if J_prod is false. */
+tt_status tt_rank(const tt_space* sp, const tt_config* cfg, uint64_t* rank);
+tt_status tt_unrank(const tt_space* sp, uint64_t rank, tt_config* out);
+
+/* J of Eq. 5: *j_prod per Eq. 2-4 + P:191 footnote; *j_hw per the family table. */
+tt_status tt_is_legitimate(const tt_space* sp, const tt_config* cfg, int32_t* j_prod, int32_t* j_hw);
+
+/* Eq. 6-7: s' = step(s, a) for a = (axis 0=m/1=k/2=n, double slot i, halve slot j).
+ * *legit = 1 if s' has J (J_prod and J_hw); s' is written only when the halved factor is even. */
+tt_status tt_step(const tt_space* sp, const tt_config* cfg, int32_t axis, int32_t i, int32_t j,
+                  tt_config* out, int32_t* legit);
+
+/* g(s) of Eq. 9 restricted to legitimate results (reading Z4), in action order
+ * (x = m,k,n; i ascending; j ascending).  At most sum_x d_x(d_x-1) (26) entries. */
+tt_status tt_neighbors(const tt_space* sp, const tt_config* cfg, tt_config* out, int32_t cap,
+                       int32_t* n_out);
+
+/* Launch binding of a feasible config (grid, block, smem, stages, descriptors). */
+tt_status tt_binding(const tt_space* sp, const tt_config* cfg, tt_launch_info* info);
+
+/* ---------------------------------------------------------------- device: generator, GEMM */
+
+/* K4: fill `count` elements with the counter-based U[-1,1) recipe of DESIGN.md §5 for matrix
+ * seed `seed` at logical indices idx0 .. idx0+count-1.  dtype 0 = fp32, 1 = bf16 (RNE).
+ * dst is device memory; launched on `stream` (cudaStream_t, null = legacy default stream). */
+tt_status tt_fill_uniform(void* dst, int32_t dtype, uint64_t seed, uint64_t idx0, uint64_t count,
+                          void* stream);
+
+/* The tiled GEMM of the paper for config cfg of family `family`:
+ * C[M][N] (fp32) = A[M][K] . B[K][N].  A/B are fp32 for F32_SIMT and TF32_UMMA, bf16 for
+ * BF16_UMMA.  Device pointers; launched on `stream`; never allocates, never synchronises.
+ * The config's trip counts must tile M, N, K exactly (J_prod) and satisfy J_hw.
+ * F32_SIMT keeps one fmaf chain per output in k order (bit-exact vs the oracle's fmaf mode).
+ * Alignment: A, B, C 16-byte aligned; UMMA families need K and N multiples of 8 (bf16) / 4. */
+tt_status tt_gemm(int64_t M, int64_t N, int64_t K, int32_t family, const void* A, const void* B,
+                  float* C, const tt_config* cfg, void* stream);
+
+/* Same product through host buffers: copies A, B host->device, runs tt_gemm, copies C back,
+ * all on the ctx stream, and synchronises.  The ctx owns the device staging buffers. */
+tt_status tt_gemm_host(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, int32_t family,
+                       const void* A_host, const void* B_host, float* C_host, const tt_config* cfg);
+
+/* ---------------------------------------------------------------- measurement (B2) */
+
+/* A context on CUDA device `device`: owns a stream, events, an L2-flush buffer and the
+ * measurement operands (generated on first use per (M,N,K,dtype) with seeds input_seed (A) and
+ * input_seed + 1 (B) by K4). */
+tt_status tt_ctx_create(int32_t device, uint64_t input_seed, tt_ctx** out);
+tt_status tt_ctx_destroy(tt_ctx* ctx);
+/* The ctx stream (cudaStream_t) -- use it to order caller work with measurements. */
+tt_status tt_ctx_stream(tt_ctx* ctx, void** stream);
+/* Device pointers of the ctx operands for this problem (created if needed). */
+tt_status tt_ctx_operands(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, int32_t family,
+                          const void** A, const void** B, float** C);
+
+/* cost(s) on hardware ("test (i.e., run the configuration on target hardware)"):
+ * warmup, one probe, then R repeats of `number` launches between CUDA events on the ctx stream;
+ * cost = median of per-repeat means (Z10).  TT_E_ILLEGITIMATE / TT_E_INFEASIBLE for a config
+ * without J; TT_E_CUDA on a launch error. */
+tt_status tt_measure(tt_ctx* ctx, const tt_space* sp, const tt_config* cfg,
+                     const tt_measure_opts* opts, tt_sample* out);
+
+/* ---------------------------------------------------------------- searches (B4) */
+
+/* G-BFS, Algorithm 1 with readings Z4-Z9.  budget_evals = max distinct states
+ * measured including s0 (0 = unlimited).  trace (nullable) receives up to trace_cap rows.
+ * TT_E_INVAL for an illegitimate s0 (before any evaluation); TT_E_EVALUATOR if the cost
+ * source fails (out and trace hold the partial search). */
+tt_status tt_gbfs_search(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, uint64_t budget_evals,
+                         const tt_search_opts* opts, tt_result* out, tt_trace_row* trace,
+                         uint64_t trace_cap);
+
+/* N-A2C, Algorithm 2 with readings Z18.  Same contract as tt_gbfs_search. */
+tt_status tt_na2c_search(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, uint64_t budget_evals,
+                         const tt_search_opts* opts, tt_result* out, tt_trace_row* trace,
+                         uint64_t trace_cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TILETUNE_H */

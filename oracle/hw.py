@@ -18,10 +18,10 @@ FAM_NONE, FAM_F32_SIMT, FAM_TF32_UMMA, FAM_BF16_UMMA = 0, 1, 2, 3
 
 # DESIGN.md §4 constants
 SMEM_PER_CTA = 232448          # 227 KB opt-in dynamic shared memory per CTA on sm_100
-SIMT_MAX_THREADS = 1024
+SIMT_SMEM_PAD = 4               # floats of padding per smem tile row (bank-conflict-free stores)
 SIMT_MAX_GROUP = 32             # m2*n2 threads form one warp-level thread group
 SIMT_MAX_ACC = 128              # m3*n3 fp32 accumulators per thread
-SIMT_MAX_REG_DIM = 64           # m3, n3 <= 64
+SIMT_MAX_REG_DIM = 64           # m3, n3 <= 64 and powers of two (compiled register tiles)
 SIMT_MAX_GRID_Y = 65535         # m0 is grid.y
 SIMT_STAGES = 2
 UMMA_M_ATOM = 128               # m3: UMMA_M per CTA
@@ -39,6 +39,23 @@ def _umma_k(family: int) -> int:
     return 8 if family == FAM_TF32_UMMA else 16
 
 
+def simt_max_threads(acc: int) -> int:
+    """Threads per CTA allowed for a register tile of ``acc`` = m3*n3 accumulators: the kernel
+    instance is compiled with __launch_bounds__ of this size so that threads x registers fits
+    the 64K-register file (255 registers at 256 threads)."""
+    return 1024 if acc <= 16 else (512 if acc <= 64 else 256)
+
+
+def umma_stage_bytes(fam: int, s) -> int:
+    """Shared memory of one pipeline stage: the A tile (m2*128 rows x k1, K-major) plus the B
+    tile (k1 rows x n2*n3/m1 columns, MN-major) rounded up to 1024 B (swizzle-atom alignment)."""
+    (m0, m1, m2, m3), (k0, k1), (n0, n1, n2, n3) = s
+    elem = _elem_bytes(fam)
+    a = m2 * UMMA_M_ATOM * k1 * elem
+    b = n2 * (n3 // m1) * k1 * elem
+    return a + (b + 1023) // 1024 * 1024
+
+
 def j_hw(spec, s) -> bool:
     fam = spec.family
     if fam == FAM_NONE:
@@ -48,16 +65,18 @@ def j_hw(spec, s) -> bool:
     (m0, m1, m2, m3), (k0, k1), (n0, n1, n2, n3) = s
     if fam == FAM_F32_SIMT:
         threads = m1 * n1 * m2 * n2
-        if threads > SIMT_MAX_THREADS:
+        if threads > simt_max_threads(m3 * n3):
             return False
         if m2 * n2 > SIMT_MAX_GROUP:
             return False
         if m3 * n3 > SIMT_MAX_ACC or m3 > SIMT_MAX_REG_DIM or n3 > SIMT_MAX_REG_DIM:
             return False
+        if m3 & (m3 - 1) or n3 & (n3 - 1):   # register tiles are compiled for powers of two
+            return False
         if m0 > SIMT_MAX_GRID_Y:
             return False
         bm, bn = m1 * m2 * m3, n1 * n2 * n3
-        return SIMT_STAGES * (bm + bn) * k1 * 4 <= SMEM_PER_CTA
+        return SIMT_STAGES * (bm + bn + 2 * SIMT_SMEM_PAD) * k1 * 4 <= SMEM_PER_CTA
     if fam in (FAM_TF32_UMMA, FAM_BF16_UMMA):
         elem = _elem_bytes(fam)
         if m3 != UMMA_M_ATOM or m1 not in (1, 2) or m2 not in (1, 2):
@@ -73,8 +92,9 @@ def j_hw(spec, s) -> bool:
             return False
         if k1 % _umma_k(fam) != 0 or k1 > UMMA_MAX_BK:
             return False
-        stage = (m2 * UMMA_M_ATOM + n2 * nb) * k1 * elem
-        return UMMA_PIPE_SMEM // stage >= UMMA_MIN_STAGES
+        if n3 & (n3 - 1) or k1 & (k1 - 1):   # TMA / UMMA swizzle widths are 32, 64 or 128 B
+            return False
+        return UMMA_PIPE_SMEM // umma_stage_bytes(fam, s) >= UMMA_MIN_STAGES
     return False
 
 

@@ -1,0 +1,68 @@
+"""Build libtiletune.so in-tree with nvcc for sm_100a (no JIT, no torch extension machinery).
+
+    python -m paper_1909_10616_b200.build [--force]
+
+Every translation unit is compiled in parallel to build/*.o, then linked into
+``paper_1909_10616_b200/libtiletune.so`` (static cudart; the CUDA driver is reached through
+cudaGetDriverEntryPoint, so no -lcuda).  Flags: -gencode arch=compute_100a,code=sm_100a
+-lineinfo -O3.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "..", "build", "tiletune")
+LIB = os.path.join(HERE, "libtiletune.so")
+INCLUDE = os.path.join(HERE, "..", "include")
+SOURCES = ["space.cpp", "search.cpp", "abi.cpp", "ctx.cu", "gemm_simt.cu", "gemm_umma.cu"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nvcc() -> str:
+    for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if c and os.path.exists(c):
+            return c
+    raise RuntimeError("nvcc not found")
+
+
+def _deps_mtime() -> float:
+    files = [os.path.join(SRC, f) for f in os.listdir(SRC)] + [os.path.join(INCLUDE, "tiletune.h"), __file__]
+    return max(os.path.getmtime(f) for f in files)
+
+
+def _compile(src: str) -> str:
+    obj = os.path.join(OBJ, src + ".o")
+    cmd = [nvcc(), "-c", os.path.join(SRC, src), "-o", obj, "-O3", "-std=c++17", "-lineinfo",
+           "-Xcompiler", "-fPIC", "-I", INCLUDE] + ARCH
+    if src.endswith(".cu"):
+        cmd += ["-Xptxas", "-v"] if os.environ.get("TT_PTXAS_VERBOSE") else []
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
+    if r.stderr.strip():
+        sys.stderr.write(r.stderr)
+    return obj
+
+
+def build(force: bool = False) -> str:
+    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _deps_mtime():
+        return LIB
+    os.makedirs(OBJ, exist_ok=True)
+    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(_compile, SOURCES))
+    tmp = LIB + ".tmp"
+    r = subprocess.run([nvcc(), "-shared", "-o", tmp] + objs + ARCH + ["-lpthread"], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed:\n{r.stderr}")
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv))

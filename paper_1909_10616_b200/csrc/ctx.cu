@@ -1,0 +1,224 @@
+// K4 generator, GEMM dispatch, and the device-timed evaluator B2 (tt_ctx / tt_measure).
+//
+// cost(s) is "the running time for the configuration s", obtained by "test (i.e., run
+// the configuration on target hardware)"; the paper averages 10 repeated trials
+// (P:369).  Here: warmup launches, one probe, then R repeats of `number` back-to-back launches
+// between CUDA events on the ctx stream; cost = median of per-repeat means (reading Z10),
+// slow candidates scored by their probe (Z12), optional L2 flush before every timed launch.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <tuple>
+#include <vector>
+
+#include "ctx.hpp"
+#include "device.hpp"
+
+namespace tt {
+
+// ---------------------------------------------------------------- K4
+namespace {
+__global__ void k4_fill(void* __restrict__ dst, int dtype, uint64_t seed, uint64_t idx0, uint64_t count) {
+  const uint64_t base = seed * 0x9E3779B97F4A7C15ull;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    uint64_t z = base + (idx0 + i + 1) * 0xD1B54A32D192ED03ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    const int32_t u = (int32_t)(z >> 40) - (1 << 23);
+    const float x = (float)u * 1.1920928955078125e-07f;   // 2^-23, exact
+    if (dtype == 0) static_cast<float*>(dst)[i] = x;
+    else static_cast<__nv_bfloat16*>(dst)[i] = __float2bfloat16_rn(x);
+  }
+}
+}  // namespace
+
+tt_status launch_fill(void* dst, int dtype, uint64_t seed, uint64_t idx0, uint64_t count, cudaStream_t stream,
+                      std::string* err) {
+  if (count == 0) return TT_OK;
+  const uint64_t blocks = std::min<uint64_t>((count + 255) / 256, 148ull * 16);
+  k4_fill<<<(unsigned)blocks, 256, 0, stream>>>(dst, dtype, seed, idx0, count);
+  return cuda_ok(cudaGetLastError(), err, "k4_fill") ? TT_OK : TT_E_CUDA;
+}
+
+tt_status bind(const Space& sp, const State& s, tt_launch_info* info, std::string* err) {
+  if (sp.family == TT_FAM_F32_SIMT) return simt_bind(sp, s, info, err);
+  if (sp.family == TT_FAM_TF32_UMMA || sp.family == TT_FAM_BF16_UMMA) return umma_bind(sp, s, info, err);
+  *err = "family has no kernel";
+  return TT_E_UNSUPPORTED;
+}
+
+tt_status launch_gemm(const Space& sp, const State& s, const void* A, const void* B, float* C, cudaStream_t stream,
+                      std::string* err) {
+  if (sp.family == TT_FAM_F32_SIMT)
+    return simt_launch(sp, s, static_cast<const float*>(A), static_cast<const float*>(B), C, stream, err);
+  if (sp.family == TT_FAM_TF32_UMMA || sp.family == TT_FAM_BF16_UMMA) return umma_launch(sp, s, A, B, C, stream, err);
+  *err = "family has no kernel";
+  return TT_E_UNSUPPORTED;
+}
+
+// ---------------------------------------------------------------- ctx
+
+Ctx::~Ctx() {
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  for (auto& o : ops) {
+    cudaFree(o.A);
+    cudaFree(o.B);
+    cudaFree(o.C);
+  }
+  cudaFree(flush);
+  cudaFree(hA);
+  cudaFree(hB);
+  cudaFree(hC);
+  for (auto e : ev) cudaEventDestroy(e);
+  if (stream) cudaStreamDestroy(stream);
+  cudaSetDevice(prev);
+}
+
+tt_status Ctx::init(std::string* err) {
+  if (!cuda_ok(cudaSetDevice(device), err, "cudaSetDevice")) return TT_E_CUDA;
+  if (!cuda_ok(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), err, "cudaStreamCreate")) return TT_E_CUDA;
+  ev.resize(2 * kMaxRepeats + 2);
+  for (auto& e : ev)
+    if (!cuda_ok(cudaEventCreate(&e), err, "cudaEventCreate")) return TT_E_CUDA;
+  return TT_OK;
+}
+
+tt_status Ctx::operands(const Space& sp, Operands** out, std::string* err) {
+  const int dtype = sp.family == TT_FAM_BF16_UMMA ? 1 : 0;
+  for (auto& o : ops)
+    if (o.M == sp.dim[0] && o.N == sp.dim[2] && o.K == sp.dim[1] && o.dtype == dtype) {
+      *out = &o;
+      return TT_OK;
+    }
+  if (ops.size() >= 2) {  // keep device memory bounded: drop the oldest problem
+    cudaFree(ops.front().A);
+    cudaFree(ops.front().B);
+    cudaFree(ops.front().C);
+    ops.erase(ops.begin());
+  }
+  Operands o;
+  o.M = sp.dim[0];
+  o.K = sp.dim[1];
+  o.N = sp.dim[2];
+  o.dtype = dtype;
+  const size_t es = dtype == 1 ? 2 : 4;
+  if (!cuda_ok(cudaSetDevice(device), err, "cudaSetDevice")) return TT_E_CUDA;
+  if (!cuda_ok(cudaMalloc(&o.A, (size_t)o.M * o.K * es), err, "cudaMalloc(A)")) return TT_E_CUDA;
+  if (!cuda_ok(cudaMalloc(&o.B, (size_t)o.K * o.N * es), err, "cudaMalloc(B)")) return TT_E_CUDA;
+  if (!cuda_ok(cudaMalloc((void**)&o.C, (size_t)o.M * o.N * 4), err, "cudaMalloc(C)")) return TT_E_CUDA;
+  tt_status st = launch_fill(o.A, dtype, seed, 0, (uint64_t)o.M * o.K, stream, err);
+  if (st == TT_OK) st = launch_fill(o.B, dtype, seed + 1, 0, (uint64_t)o.K * o.N, stream, err);
+  if (st != TT_OK) return st;
+  if (!cuda_ok(cudaMemsetAsync(o.C, 0, (size_t)o.M * o.N * 4, stream), err, "memset C")) return TT_E_CUDA;
+  ops.push_back(o);
+  *out = &ops.back();
+  return TT_OK;
+}
+
+tt_status Ctx::flush_l2(std::string* err) {
+  if (!flush) {
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device);
+    flush_bytes = std::max<size_t>((size_t)l2 * 2, (size_t)256 << 20);
+    if (!cuda_ok(cudaMalloc(&flush, flush_bytes), err, "cudaMalloc(flush)")) return TT_E_CUDA;
+  }
+  ++flush_gen;
+  return cuda_ok(cudaMemsetAsync(flush, (int)(flush_gen & 0xFF), flush_bytes, stream), err, "L2 flush") ? TT_OK
+                                                                                                       : TT_E_CUDA;
+}
+
+tt_status Ctx::measure(const Space& sp, const State& s, const tt_measure_opts& mo, tt_sample* out,
+                       std::string* err) {
+  Operands* o = nullptr;
+  tt_status st = operands(sp, &o, err);
+  if (st != TT_OK) return st;
+  auto launch = [&]() { return launch_gemm(sp, s, o->A, o->B, o->C, stream, err); };
+  const int warm = mo.warmup >= 0 ? mo.warmup : 2;
+  for (int w = 0; w < warm; ++w)
+    if ((st = launch()) != TT_OK) return st;
+  if (mo.l2_flush && (st = flush_l2(err)) != TT_OK) return st;
+  cudaEventRecord(ev[0], stream);
+  if ((st = launch()) != TT_OK) return st;
+  cudaEventRecord(ev[1], stream);
+  if (!cuda_ok(cudaEventSynchronize(ev[1]), err, "probe")) return TT_E_CUDA;
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ev[0], ev[1]);
+  const double probe = ms * 1e-3;
+  *out = tt_sample{};
+  out->probe_s = probe;
+  out->device = device;
+  if (mo.cut_s > 0 && probe > mo.cut_s) {  // Z12
+    out->cost_s = out->mean_s = out->min_s = probe;
+    out->repeats = 1;
+    out->number = 1;
+    out->slow_cut = 1;
+    return TT_OK;
+  }
+  const int R = std::max(1, std::min(mo.repeats > 0 ? mo.repeats : 10, kMaxRepeats));
+  int number = 1;
+  if (!mo.l2_flush) {
+    const double mr = mo.min_repeat_s > 0 ? mo.min_repeat_s : 5e-4;
+    number = (int)std::ceil(mr / std::max(probe, 1e-9));
+    number = std::max(1, std::min(number, mo.max_number > 0 ? mo.max_number : 1000));
+  }
+  for (int r = 0; r < R; ++r) {
+    if (mo.l2_flush && (st = flush_l2(err)) != TT_OK) return st;
+    cudaEventRecord(ev[2 + 2 * r], stream);
+    for (int i = 0; i < number; ++i)
+      if ((st = launch()) != TT_OK) return st;
+    cudaEventRecord(ev[3 + 2 * r], stream);
+  }
+  if (!cuda_ok(cudaEventSynchronize(ev[1 + 2 * R]), err, "measure")) return TT_E_CUDA;
+  std::vector<double> per(R);
+  for (int r = 0; r < R; ++r) {
+    cudaEventElapsedTime(&ms, ev[2 + 2 * r], ev[3 + 2 * r]);
+    per[r] = ms * 1e-3 / number;
+  }
+  std::vector<double> srt = per;
+  std::sort(srt.begin(), srt.end());
+  double mean = 0;
+  for (double x : per) mean += x;
+  mean /= R;
+  double var = 0;
+  for (double x : per) var += (x - mean) * (x - mean);
+  out->cost_s = R % 2 ? srt[R / 2] : 0.5 * (srt[R / 2 - 1] + srt[R / 2]);
+  out->mean_s = mean;
+  out->min_s = srt[0];
+  out->stdev_s = R > 1 ? std::sqrt(var / (R - 1)) : 0.0;
+  out->repeats = R;
+  out->number = number;
+  return cuda_ok(cudaGetLastError(), err, "measure") ? TT_OK : TT_E_CUDA;
+}
+
+tt_status Ctx::gemm_host(const Space& sp, const State& s, const void* Ah, const void* Bh, float* Ch,
+                         std::string* err) {
+  const size_t es = sp.family == TT_FAM_BF16_UMMA ? 2 : 4;
+  const size_t a = (size_t)sp.dim[0] * sp.dim[1] * es, b = (size_t)sp.dim[1] * sp.dim[2] * es,
+               c = (size_t)sp.dim[0] * sp.dim[2] * 4;
+  if (!cuda_ok(cudaSetDevice(device), err, "cudaSetDevice")) return TT_E_CUDA;
+  auto grow = [&](void** p, size_t* cap, size_t need) {
+    if (*cap >= need) return true;
+    cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    if (!cuda_ok(cudaMalloc(p, need), err, "cudaMalloc(host staging)")) return false;
+    *cap = need;
+    return true;
+  };
+  if (!grow(&hA, &hAcap, a) || !grow(&hB, &hBcap, b) || !grow(&hC, &hCcap, c)) return TT_E_CUDA;
+  if (!cuda_ok(cudaMemcpyAsync(hA, Ah, a, cudaMemcpyHostToDevice, stream), err, "H2D A")) return TT_E_CUDA;
+  if (!cuda_ok(cudaMemcpyAsync(hB, Bh, b, cudaMemcpyHostToDevice, stream), err, "H2D B")) return TT_E_CUDA;
+  tt_status st = launch_gemm(sp, s, hA, hB, static_cast<float*>(hC), stream, err);
+  if (st != TT_OK) return st;
+  if (!cuda_ok(cudaMemcpyAsync(Ch, hC, c, cudaMemcpyDeviceToHost, stream), err, "D2H C")) return TT_E_CUDA;
+  return cuda_ok(cudaStreamSynchronize(stream), err, "gemm_host sync") ? TT_OK : TT_E_CUDA;
+}
+
+}  // namespace tt

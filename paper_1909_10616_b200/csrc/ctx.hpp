@@ -1,0 +1,45 @@
+// tt_ctx: per-device measurement context (B2).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "space.hpp"
+
+struct tt_ctx {};  // opaque ABI handle; tt::Ctx derives from it
+
+namespace tt {
+
+constexpr int kMaxRepeats = 64;
+
+struct Operands {
+  int64_t M = 0, N = 0, K = 0;
+  int dtype = 0;  // 0 fp32, 1 bf16
+  void* A = nullptr;
+  void* B = nullptr;
+  float* C = nullptr;
+};
+
+struct Ctx : tt_ctx {
+  int device = 0;
+  uint64_t seed = 1;
+  cudaStream_t stream = nullptr;
+  std::vector<cudaEvent_t> ev;
+  std::vector<Operands> ops;
+  void* flush = nullptr;
+  size_t flush_bytes = 0;
+  uint64_t flush_gen = 0;
+  void *hA = nullptr, *hB = nullptr, *hC = nullptr;
+  size_t hAcap = 0, hBcap = 0, hCcap = 0;
+
+  ~Ctx();
+  tt_status init(std::string* err);
+  tt_status operands(const Space& sp, Operands** out, std::string* err);
+  tt_status flush_l2(std::string* err);
+  tt_status measure(const Space& sp, const State& s, const tt_measure_opts& mo, tt_sample* out, std::string* err);
+  tt_status gemm_host(const Space& sp, const State& s, const void* Ah, const void* Bh, float* Ch, std::string* err);
+};
+
+}  // namespace tt

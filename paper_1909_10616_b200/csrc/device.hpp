@@ -1,0 +1,38 @@
+// Device-side entry points of libtiletune (kernel launchers; no torch types anywhere).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "space.hpp"
+
+namespace tt {
+
+// Launch binding (a5 of SURVEY §8a): factors -> grid, block, smem, stages, descriptors.
+tt_status bind(const Space& sp, const State& s, tt_launch_info* info, std::string* err);
+
+// K1 / K2 / K3 dispatch for a feasible config; asynchronous on `stream`.
+tt_status launch_gemm(const Space& sp, const State& s, const void* A, const void* B, float* C,
+                      cudaStream_t stream, std::string* err);
+
+// K4: counter-based U[-1,1) operand generator.
+tt_status launch_fill(void* dst, int dtype, uint64_t seed, uint64_t idx0, uint64_t count,
+                      cudaStream_t stream, std::string* err);
+
+// Family-specific launchers (gemm_simt.cu, gemm_umma.cu).
+tt_status simt_bind(const Space& sp, const State& s, tt_launch_info* info, std::string* err);
+tt_status simt_launch(const Space& sp, const State& s, const float* A, const float* B, float* C,
+                      cudaStream_t stream, std::string* err);
+tt_status umma_bind(const Space& sp, const State& s, tt_launch_info* info, std::string* err);
+tt_status umma_launch(const Space& sp, const State& s, const void* A, const void* B, float* C,
+                      cudaStream_t stream, std::string* err);
+
+inline bool cuda_ok(cudaError_t e, std::string* err, const char* what) {
+  if (e == cudaSuccess) return true;
+  *err = std::string(what) + ": " + cudaGetErrorString(e);
+  return false;
+}
+
+}  // namespace tt

@@ -1,0 +1,272 @@
+// K1: fp32 CUDA-core tiled GEMM family, parameterised by the paper's per-axis split factors.
+//
+// PAPER.md P:124-125 ("iteratively splitting computation into smaller tiles ... A resulted
+// matrix is initialized with zeros ... accumulates"), P:166 (m_i, k_l, n_j are loop trip
+// counts), P:369 (d_m = 4, d_k = 2, d_n = 4).  Level mapping (reading Z2):
+//   m = [m0 CTAs along M (grid.y), m1 thread groups per CTA along M, m2 lanes per group along
+//        M, m3 register rows per thread]
+//   n = [n0 CTAs along N (grid.x), n1 groups along N, n2 lanes along N, n3 register columns]
+//   k = [k0 main-loop trips, k1 = BK (shared-memory K slab)]
+// so the CTA tile is BM x BN = (m1 m2 m3) x (n1 n2 n3) and a thread owns an m3 x n3 register
+// tile.  Each output element is one fmaf chain in ascending k (no split-K, no k-interleaved
+// partial sums): the result is bit-identical to the oracle's sequential fmaf reference.
+//
+// B200 mapping: A/B slabs are staged global -> shared with cp.async (LDGSTS), double
+// buffered (2 stages) so the next slab's copy overlaps the FFMA work on the current one; A is
+// transposed on the way in (As[k][m], rows padded by 4 floats so the strided LDGSTS stores are
+// bank-conflict free for BK = 8 warps); register tiles are read with LDS.128 when m3/n3 are
+// multiples of 4 and results are stored with STG.128.
+#include <cuda_runtime.h>
+
+#include "device.hpp"
+
+namespace tt {
+
+namespace {
+
+struct SimtArgs {
+  const float* A;
+  const float* B;
+  float* C;
+  int64_t M, N, K;
+  int m1, m2, n1, n2, bk, k0;
+  int a_vec;  // As base 16-byte aligned (float4 reads legal)
+  int b_vec;  // B rows 16-byte aligned (16-byte cp.async legal)
+};
+
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(float* dst, const float* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <int ACC>
+struct MaxThreads {
+  static constexpr int value = ACC <= 16 ? 1024 : (ACC <= 64 ? 512 : 256);
+};
+
+template <int TM, int TN>
+__global__ void __launch_bounds__(MaxThreads<TM * TN>::value)
+k1_simt(SimtArgs p) {
+  extern __shared__ __align__(16) float smem[];
+  const int BM = p.m1 * p.m2 * TM;
+  const int BN = p.n1 * p.n2 * TN;
+  const int BK = p.bk;
+  const int LDA = BM + 4, LDB = BN + 4;
+  float* Bs = smem;                      // [2][BK][LDB]
+  float* As = smem + 2 * BK * LDB;       // [2][BK][LDA]
+
+  const int T = blockDim.x;
+  const int t = threadIdx.x;
+  const int G = p.m2 * p.n2;
+  const int g = t / G, l = t - (t / G) * G;
+  const int gm = g / p.n1, gn = g - (g / p.n1) * p.n1;
+  const int lm = l / p.n2, ln = l - (l / p.n2) * p.n2;
+  const int row0 = gm * (p.m2 * TM) + lm * TM;
+  const int col0 = gn * (p.n2 * TN) + ln * TN;
+
+  const int64_t K = p.K, N = p.N;
+  const float* Ab = p.A + (int64_t)blockIdx.y * BM * K;
+  const float* Bb = p.B + (int64_t)blockIdx.x * BN;
+
+  auto load = [&](int kt, int buf) {
+    float* as = As + buf * BK * LDA;
+    float* bs = Bs + buf * BK * LDB;
+    const int64_t kb = (int64_t)kt * BK;
+    const int na = BM * BK;
+    for (int e = t; e < na; e += T) {
+      const int r = e / BK, c = e - (e / BK) * BK;
+      cp_async4(as + c * LDA + r, Ab + (int64_t)r * K + kb + c);
+    }
+    if (p.b_vec) {
+      const int q = BN >> 2;
+      const int nb = BK * q;
+      for (int e = t; e < nb; e += T) {
+        const int r = e / q, c = (e - (e / q) * q) << 2;
+        cp_async16(bs + r * LDB + c, Bb + (kb + r) * N + c);
+      }
+    } else {
+      const int nb = BK * BN;
+      for (int e = t; e < nb; e += T) {
+        const int r = e / BN, c = e - (e / BN) * BN;
+        cp_async4(bs + r * LDB + c, Bb + (kb + r) * N + c);
+      }
+    }
+  };
+
+  float acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;
+
+  load(0, 0);
+  cp_async_commit();
+  for (int kt = 0; kt < p.k0; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < p.k0) {
+      load(kt + 1, buf ^ 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const float* as = As + buf * BK * LDA + row0;
+    const float* bs = Bs + buf * BK * LDB + col0;
+#pragma unroll 2
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[TM], b[TN];
+      if constexpr (TM % 4 == 0) {
+        if (p.a_vec) {
+#pragma unroll
+          for (int i = 0; i < TM; i += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(as + kk * LDA + i);
+            a[i] = v.x; a[i + 1] = v.y; a[i + 2] = v.z; a[i + 3] = v.w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < TM; ++i) a[i] = as[kk * LDA + i];
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < TM; ++i) a[i] = as[kk * LDA + i];
+      }
+      if constexpr (TN % 4 == 0) {
+#pragma unroll
+        for (int j = 0; j < TN; j += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(bs + kk * LDB + j);
+          b[j] = v.x; b[j + 1] = v.y; b[j + 2] = v.z; b[j + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < TN; ++j) b[j] = bs[kk * LDB + j];
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+
+  float* Cb = p.C + ((int64_t)blockIdx.y * BM + row0) * N + (int64_t)blockIdx.x * BN + col0;
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    if constexpr (TN % 4 == 0) {
+      if ((N & 3) == 0) {
+#pragma unroll
+        for (int j = 0; j < TN; j += 4)
+          *reinterpret_cast<float4*>(Cb + i * N + j) = make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+        continue;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < TN; ++j) Cb[i * N + j] = acc[i][j];
+  }
+}
+
+using KernelFn = void (*)(SimtArgs);
+
+template <int LM, int LN>
+constexpr KernelFn kfn() {
+  if constexpr ((1 << LM) * (1 << LN) <= 128) return &k1_simt<(1 << LM), (1 << LN)>;
+  else return nullptr;
+}
+
+template <int LM, int... LNs>
+constexpr void fill_row(KernelFn (&t)[7][7], std::integer_sequence<int, LNs...>) {
+  ((t[LM][LNs] = kfn<LM, LNs>()), ...);
+}
+template <int... LMs>
+constexpr void fill_all(KernelFn (&t)[7][7], std::integer_sequence<int, LMs...>) {
+  (fill_row<LMs>(t, std::make_integer_sequence<int, 7>{}), ...);
+}
+
+struct Table {
+  KernelFn fn[7][7] = {};
+  bool attr_set[7][7] = {};
+  Table() { fill_all(fn, std::make_integer_sequence<int, 7>{}); }
+};
+Table& table() {
+  static Table t;
+  return t;
+}
+
+int ilog2(int64_t v) {
+  int l = 0;
+  while ((int64_t(1) << l) < v) ++l;
+  return l;
+}
+
+}  // namespace
+
+tt_status simt_bind(const Space& sp, const State& s, tt_launch_info* info, std::string* err) {
+  const int64_t m0 = s.f[0][0], m1 = s.f[0][1], m2 = s.f[0][2], m3 = s.f[0][3];
+  const int64_t k1 = s.f[1][1];
+  const int64_t n0 = s.f[2][0], n1 = s.f[2][1], n2 = s.f[2][2], n3 = s.f[2][3];
+  *info = tt_launch_info{};
+  info->family = TT_FAM_F32_SIMT;
+  info->grid_x = n0;
+  info->grid_y = m0;
+  info->grid_z = 1;
+  info->block_x = (int32_t)(m1 * n1 * m2 * n2);
+  info->cluster_x = 1;
+  info->smem_bytes = (int32_t)(kSimtStages * (m1 * m2 * m3 + n1 * n2 * n3 + 2 * kSimtPad) * k1 * 4);
+  info->stages = kSimtStages;
+  info->tile_m = (int32_t)(m1 * m2 * m3);
+  info->tile_n = (int32_t)(n1 * n2 * n3);
+  info->tile_k = (int32_t)k1;
+  info->reg_tile_m = (int32_t)m3;
+  info->reg_tile_n = (int32_t)n3;
+  (void)sp;
+  (void)err;
+  return TT_OK;
+}
+
+tt_status simt_launch(const Space& sp, const State& s, const float* A, const float* B, float* C,
+                      cudaStream_t stream, std::string* err) {
+  tt_launch_info li;
+  simt_bind(sp, s, &li, err);
+  const int lm = ilog2(li.reg_tile_m), ln = ilog2(li.reg_tile_n);
+  Table& tb = table();
+  KernelFn fn = tb.fn[lm][ln];
+  if (!fn) {
+    *err = "no SIMT kernel instance for this register tile";
+    return TT_E_UNSUPPORTED;
+  }
+  if (!tb.attr_set[lm][ln]) {
+    if (!cuda_ok(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemPerCta),
+                 err, "cudaFuncSetAttribute(k1_simt)"))
+      return TT_E_CUDA;
+    tb.attr_set[lm][ln] = true;
+  }
+  SimtArgs a;
+  a.A = A;
+  a.B = B;
+  a.C = C;
+  a.M = sp.dim[0];
+  a.K = sp.dim[1];
+  a.N = sp.dim[2];
+  a.m1 = (int)s.f[0][1];
+  a.m2 = (int)s.f[0][2];
+  a.n1 = (int)s.f[2][1];
+  a.n2 = (int)s.f[2][2];
+  a.bk = (int)s.f[1][1];
+  a.k0 = (int)s.f[1][0];
+  const int64_t LDB = li.tile_n + 4;
+  a.a_vec = ((2 * (int64_t)a.bk * LDB) % 4 == 0) ? 1 : 0;
+  a.b_vec = (li.tile_n % 4 == 0 && a.N % 4 == 0 && ((uintptr_t)B % 16) == 0) ? 1 : 0;
+  dim3 grid((unsigned)li.grid_x, (unsigned)li.grid_y, 1);
+  fn<<<grid, li.block_x, li.smem_bytes, stream>>>(a);
+  if (!cuda_ok(cudaGetLastError(), err, "k1_simt launch")) return TT_E_CUDA;
+  return TT_OK;
+}
+
+}  // namespace tt

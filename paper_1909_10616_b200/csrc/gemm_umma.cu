@@ -1,0 +1,529 @@
+// K2 / K3: tcgen05 (5th-gen tensor core) tiled GEMM family for sm_100a, TF32 and BF16.
+//
+// The paper's tiling configuration (Eq. 1-4; d = (4,2,4)) is bound to a
+// persistent, warp-specialised tcgen05 kernel (reading Z2):
+//   m = [m0 cluster tiles along M, m1 = cta_group (1, or 2 = CTA pair sharing one UMMA_M=256
+//        instruction), m2 = UMMA M-atoms per CTA (1|2), m3 = UMMA_M per CTA (128)]
+//   n = [n0 cluster tiles along N, n1 = 1, n2 = UMMA N-atoms per CTA (1|2), n3 = UMMA_N]
+//   k = [k0 main-loop trips, k1 = BK (K slab per pipeline stage)]
+// Cluster tile = (m1 m2 128) x (n2 n3).  C[M][N] fp32 = A[M][K] . B[K][N] with A K-major and
+// B MN-major (row-major B is read transposed by the descriptor; no copy).
+//
+// Warp roles (256 threads, 1 CTA per SM): warp 0 = TMA producer (A and B slabs into a
+// `stages`-deep shared-memory ring guarded by full/empty mbarriers), warp 1 = MMA issuer
+// (one elected thread, leader CTA only), warp 2 = TMEM allocator, warps 4-7 = epilogue
+// (TMEM -> registers via tcgen05.ld -> global fp32 C).  Accumulators are double buffered in
+// TMEM when m2 n2 n3 <= 256 columns so the epilogue of tile t overlaps the MMAs of tile t+1.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "device.hpp"
+
+namespace tt {
+
+namespace {
+
+struct UmmaArgs {
+  int64_t M, N, K;
+  int m0, n0, k0;
+  int m2, n2, n3, bk;
+  int stages, acc_bufs, acc_cols;   // acc_cols = m2 n2 n3 (columns per accumulator buffer)
+  int tmem_cols;
+  int swz_a, swz_b;                 // swizzle bytes: 32 | 64 | 128
+  int a_chunk_bytes;                // bytes of one A K-chunk (rows x swz_a)
+  int b_cw;                         // B columns per TMA box (swz_b / elem)
+  int nb;                           // B columns per CTA per atom = n3 / cta_group
+  int a_stage_bytes, stage_bytes;   // A part, total per stage (A + padded B)
+  uint32_t idesc;
+  uint32_t tx_bytes;                // bytes landing per stage per CTA
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}" : "=r"(ok) : "r"(bar), "r"(parity), "r"(0x989680) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Watchdog: a pipeline that has not advanced for 10 s traps (a launch error the host reports)
+// instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  if (mbar_try(bar, parity)) return;
+  const uint64_t t0 = globaltimer();
+  while (!mbar_try(bar, parity)) {
+    if (globaltimer() - t0 > 10000000000ull) __trap();
+  }
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(bar), "r"(cta) : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int CG>
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint32_t bar, uint32_t dst, int x, int y) {
+  if constexpr (CG == 1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(dst), "l"(map), "r"(x), "r"(y), "r"(bar) : "memory");
+  } else {
+    // both CTAs of the pair signal the leader's barrier (peer bit cleared)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(dst), "l"(map), "r"(x), "r"(y), "r"(bar & 0xFEFFFFFFu) : "memory");
+  }
+}
+
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, int swz) {
+  // tcgen05 shared-memory matrix descriptor: start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46),
+  // version 1 [46,48), base offset 0, layout [61,64): SW128 = 2, SW64 = 4, SW32 = 6
+  const uint64_t layout = swz == 128 ? 2ull : (swz == 64 ? 4ull : 6ull);
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (layout << 61);
+}
+
+template <int KIND, int CG>
+__device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (KIND == 0 && CG == 1)
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                 ::"r"(d_tmem), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+  else if constexpr (KIND == 0 && CG == 2)
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                 ::"r"(d_tmem), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+  else if constexpr (KIND == 1 && CG == 1)
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+                 ::"r"(d_tmem), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+  else
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+                 ::"r"(d_tmem), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+template <int CG>
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  if constexpr (CG == 1)
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+  else
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(bar), "h"((uint16_t)0x3) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ---------------------------------------------------------------- the kernel
+template <int KIND, int CG>
+__global__ void __launch_bounds__(256, 1)
+k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, float* __restrict__ C,
+       const UmmaArgs p) {
+  constexpr int ELEM = KIND == 0 ? 2 : 4;
+  constexpr int UK = KIND == 0 ? 16 : 8;     // UMMA_K
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)p.stages * p.stage_bytes);
+  const uint32_t full0 = smem_u32(bars);
+  const uint32_t empty0 = full0 + 8u * p.stages;
+  const uint32_t tfull0 = empty0 + 8u * p.stages;
+  const uint32_t tempty0 = tfull0 + 16u;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * p.stages + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+  const bool leader = rank == 0;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(full0 + 8u * s, CG);
+      mbar_init(empty0 + 8u * s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull0 + 8u * b, 1);
+      mbar_init(tempty0 + 8u * b, 4 * CG);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    if constexpr (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(p.tmem_cols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(p.tmem_cols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+  }
+  tc_fence_before();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_tiles = p.m0 * p.n0;
+  const int cluster_id = blockIdx.x / CG;
+  const int num_clusters = gridDim.x / CG;
+  const int rows_cta = p.m2 * 128;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer =====
+      int stage = 0;
+      uint32_t phase = 0;
+      const int kchunks = p.bk * ELEM / p.swz_a;
+      const int bboxes = p.nb / p.b_cw;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+        const int tm = tile % p.m0, tn = tile / p.m0;
+        const int row = tm * (CG * rows_cta) + (int)rank * rows_cta;
+        const int colt = tn * (p.n2 * p.n3) + (int)rank * p.nb;
+        for (int kb = 0; kb < p.k0; ++kb) {
+          mbar_wait(empty0 + 8u * stage, phase ^ 1u);
+          const uint32_t fb = full0 + 8u * stage;
+          if (leader) mbar_arrive_expect_tx(fb, p.tx_bytes * CG);
+          const uint32_t sa = sbase + (uint32_t)stage * p.stage_bytes;
+          const uint32_t sb = sa + p.a_stage_bytes;
+          for (int kc = 0; kc < kchunks; ++kc)
+            tma_load_2d<CG>(&tmA, fb, sa + kc * p.a_chunk_bytes, kb * p.bk + kc * (p.swz_a / ELEM), row);
+          for (int ni = 0; ni < p.n2; ++ni)
+            for (int c = 0; c < bboxes; ++c)
+              tma_load_2d<CG>(&tmB, fb, sb + (uint32_t)((ni * bboxes + c) * p.bk * p.swz_b),
+                              colt + ni * p.n3 + c * p.b_cw, kb * p.bk);
+          if (CG == 2 && !leader) mbar_arrive_cluster(fb, 0);
+          if (++stage == p.stages) { stage = 0; phase ^= 1u; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // ===== MMA issuer =====
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      const int ksteps = p.bk / UK;
+      const int bboxes = p.nb / p.b_cw;
+      const uint32_t sbo_a = 8u * p.swz_a;
+      const uint32_t lbo_b = (uint32_t)(p.bk * p.swz_b), sbo_b = 8u * p.swz_b;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+        mbar_wait(tempty0 + 8u * acc, aphase ^ 1u);
+        tc_fence_after();
+        const uint32_t dbase = tmem_base + (uint32_t)(acc * p.acc_cols);
+        for (int kb = 0; kb < p.k0; ++kb) {
+          mbar_wait(full0 + 8u * stage, phase);
+          tc_fence_after();
+          const uint32_t sa = sbase + (uint32_t)stage * p.stage_bytes;
+          const uint32_t sb = sa + p.a_stage_bytes;
+          for (int ks = 0; ks < ksteps; ++ks) {
+            const uint32_t kbytes = (uint32_t)(ks * UK * ELEM);
+            const uint32_t a_off = (kbytes / p.swz_a) * p.a_chunk_bytes + (kbytes % p.swz_a);
+            for (int mi = 0; mi < p.m2; ++mi) {
+              const uint64_t ad = smem_desc(sa + a_off + (uint32_t)(mi * 128 * p.swz_a), 16u, sbo_a, p.swz_a);
+              for (int ni = 0; ni < p.n2; ++ni) {
+                const uint64_t bd = smem_desc(sb + (uint32_t)(ni * bboxes) * lbo_b + (uint32_t)(ks * UK * p.swz_b),
+                                              lbo_b, sbo_b, p.swz_b);
+                umma<KIND, CG>(dbase + (uint32_t)((mi * p.n2 + ni) * p.n3), ad, bd, p.idesc,
+                               (kb | ks) != 0 ? 1u : 0u);
+              }
+            }
+          }
+          umma_commit<CG>(empty0 + 8u * stage);           // frees the smem slot when MMAs finish
+          if (++stage == p.stages) { stage = 0; phase ^= 1u; }
+        }
+        umma_commit<CG>(tfull0 + 8u * acc);                // accumulator ready for the epilogue
+        if (++acc == p.acc_bufs) { acc = 0; aphase ^= 1u; }
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== epilogue: TMEM -> registers -> global =====
+    const int q = warp & 3;                                // TMEM lanes [32q, 32q+32)
+    int acc = 0;
+    uint32_t aphase = 0;
+    float v[32];
+    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+      const int tm = tile % p.m0, tn = tile / p.m0;
+      mbar_wait(tfull0 + 8u * acc, aphase);
+      tc_fence_after();
+      const int64_t row_cta = (int64_t)tm * (CG * rows_cta) + (int64_t)rank * rows_cta;
+      for (int mi = 0; mi < p.m2; ++mi) {
+        const int64_t row = row_cta + mi * 128 + q * 32 + lane;
+        float* crow = C + row * p.N + (int64_t)tn * (p.n2 * p.n3);
+        for (int ni = 0; ni < p.n2; ++ni) {
+          const uint32_t tcol = (uint32_t)(acc * p.acc_cols + (mi * p.n2 + ni) * p.n3);
+          const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + tcol;
+          int c0 = 0;
+          for (; c0 + 32 <= p.n3; c0 += 32) {
+            tmem_ld32(taddr + (uint32_t)c0, v);
+            float4* dst = reinterpret_cast<float4*>(crow + ni * p.n3 + c0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
+          if (c0 < p.n3) {                                 // n3 = 16 (UMMA_N multiple of 16)
+            tmem_ld16(taddr + (uint32_t)c0, v);
+            float4* dst = reinterpret_cast<float4*>(crow + ni * p.n3 + c0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (CG == 1 || leader) mbar_arrive(tempty0 + 8u * acc);
+        else mbar_arrive_cluster(tempty0 + 8u * acc, 0);
+      }
+      if (++acc == p.acc_bufs) { acc = 0; aphase ^= 1u; }
+    }
+  }
+
+  __syncwarp();                                            // reconverge role warps
+  tc_fence_before();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  tc_fence_after();
+  if (warp == 2) {
+    if constexpr (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(p.tmem_cols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(p.tmem_cols));
+  }
+}
+
+// ---------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn(std::string* err) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  if (!fn) *err = "cuTensorMapEncodeTiled unavailable";
+  return fn;
+}
+
+CUtensorMapSwizzle swz_enum(int s) {
+  return s == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : (s == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+}
+
+bool make_map(CUtensorMap* m, int kind, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_in,
+              uint32_t box_out, int swz, std::string* err) {
+  auto fn = encode_fn(err);
+  if (!fn) return false;
+  const int elem = kind == 0 ? 2 : 4;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * (uint64_t)elem};
+  cuuint32_t box[2] = {box_in, box_out};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, kind == 0 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                  const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz_enum(swz),
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    *err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
+    return false;
+  }
+  return true;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+struct Plan {
+  UmmaArgs a;
+  int cg, kind;
+  int grid;
+  int smem;
+};
+
+void plan_of(const Space& sp, const State& s, Plan* pl) {
+  const int fam = sp.family;
+  const int kind = fam == TT_FAM_BF16_UMMA ? 0 : 1;
+  const int elem = kind == 0 ? 2 : 4;
+  UmmaArgs& a = pl->a;
+  std::memset(&a, 0, sizeof(a));
+  a.M = sp.dim[0];
+  a.K = sp.dim[1];
+  a.N = sp.dim[2];
+  const int m1 = (int)s.f[0][1];
+  a.m0 = (int)s.f[0][0];
+  a.m2 = (int)s.f[0][2];
+  a.k0 = (int)s.f[1][0];
+  a.bk = (int)s.f[1][1];
+  a.n0 = (int)s.f[2][0];
+  a.n2 = (int)s.f[2][2];
+  a.n3 = (int)s.f[2][3];
+  a.nb = a.n3 / m1;
+  a.swz_a = std::min(a.bk * elem, 128);
+  a.swz_b = std::min(a.nb * elem, 128);
+  a.b_cw = a.swz_b / elem;
+  a.a_chunk_bytes = a.m2 * 128 * a.swz_a;
+  a.a_stage_bytes = a.m2 * 128 * a.bk * elem;
+  a.stage_bytes = (int)umma_stage_bytes(fam, s);
+  a.tx_bytes = (uint32_t)(a.a_stage_bytes + a.n2 * a.nb * a.bk * elem);
+  a.stages = std::min<int>(kUmmaMaxStages, kUmmaPipeSmem / a.stage_bytes);
+  a.acc_cols = a.m2 * a.n2 * a.n3;
+  a.acc_bufs = a.acc_cols <= 256 ? 2 : 1;
+  int need = a.acc_cols * a.acc_bufs, cols = 32;
+  while (cols < need) cols <<= 1;
+  a.tmem_cols = cols;
+  // instruction descriptor: F32 accum, A/B format, A K-major, B MN-major, N>>3, M>>4
+  const uint32_t fmt = kind == 0 ? 1u : 2u;
+  const uint32_t M_inst = 128u * (uint32_t)m1;
+  a.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (0u << 15) | (1u << 16) | (((uint32_t)a.n3 >> 3) << 17) |
+            ((M_inst >> 4) << 24);
+  pl->cg = m1;
+  pl->kind = kind;
+  const int tiles = a.m0 * a.n0;
+  const int max_clusters = num_sms() / m1;
+  pl->grid = std::min(tiles, max_clusters) * m1;
+  pl->smem = a.stages * a.stage_bytes + 1024 /*align*/ + 8 * (2 * a.stages + 4) + 16;
+}
+
+template <int KIND, int CG>
+tt_status launch_t(const Plan& pl, const CUtensorMap& ma, const CUtensorMap& mb, float* C, cudaStream_t stream,
+                   std::string* err) {
+  auto fn = &k_umma<KIND, CG>;
+  static bool attr = false;
+  if (!attr) {
+    if (!cuda_ok(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemPerCta), err,
+                 "cudaFuncSetAttribute(k_umma)"))
+      return TT_E_CUDA;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)pl.grid, 1, 1);
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.dynamicSmemBytes = (size_t)pl.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = CG;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  if (!cuda_ok(cudaLaunchKernelEx(&cfg, fn, ma, mb, C, pl.a), err, "k_umma launch")) return TT_E_CUDA;
+  return TT_OK;
+}
+
+}  // namespace
+
+tt_status umma_bind(const Space& sp, const State& s, tt_launch_info* info, std::string* err) {
+  Plan pl;
+  plan_of(sp, s, &pl);
+  *info = tt_launch_info{};
+  info->family = sp.family;
+  info->grid_x = pl.grid;
+  info->grid_y = 1;
+  info->grid_z = 1;
+  info->block_x = 256;
+  info->cluster_x = pl.cg;
+  info->smem_bytes = pl.smem;
+  info->stages = pl.a.stages;
+  info->tile_m = pl.cg * pl.a.m2 * 128;
+  info->tile_n = pl.a.n2 * pl.a.n3;
+  info->tile_k = pl.a.bk;
+  info->tmem_cols = pl.a.tmem_cols;
+  info->acc_buffers = pl.a.acc_bufs;
+  info->idesc = pl.a.idesc;
+  (void)err;
+  return TT_OK;
+}
+
+tt_status umma_launch(const Space& sp, const State& s, const void* A, const void* B, float* C, cudaStream_t stream,
+                      std::string* err) {
+  Plan pl;
+  plan_of(sp, s, &pl);
+  if (((uintptr_t)A % 16) || ((uintptr_t)B % 16) || ((uintptr_t)C % 16)) {
+    *err = "UMMA family needs 16-byte aligned A, B, C";
+    return TT_E_INVAL;
+  }
+  const int elem = pl.kind == 0 ? 2 : 4;
+  if ((pl.a.K * elem) % 16 || (pl.a.N * elem) % 16) {
+    *err = "UMMA family needs row pitches that are multiples of 16 bytes";
+    return TT_E_UNSUPPORTED;
+  }
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, pl.kind, A, (uint64_t)pl.a.K, (uint64_t)pl.a.M, (uint32_t)(pl.a.swz_a / elem),
+                (uint32_t)(pl.a.m2 * 128), pl.a.swz_a, err))
+    return TT_E_CUDA;
+  if (!make_map(&mb, pl.kind, B, (uint64_t)pl.a.N, (uint64_t)pl.a.K, (uint32_t)pl.a.b_cw, (uint32_t)pl.a.bk,
+                pl.a.swz_b, err))
+    return TT_E_CUDA;
+  if (pl.kind == 0) {
+    return pl.cg == 1 ? launch_t<0, 1>(pl, ma, mb, C, stream, err) : launch_t<0, 2>(pl, ma, mb, C, stream, err);
+  }
+  return pl.cg == 1 ? launch_t<1, 1>(pl, ma, mb, C, stream, err) : launch_t<1, 2>(pl, ma, mb, C, stream, err);
+}
+
+}  // namespace tt

@@ -1,0 +1,262 @@
+"""GPU parity of the CUDA path (through the C-ABI) against the oracle.  Run with -m gpu on a B200.
+
+Tolerances (north star; reading Z15 normwise max|C - R| / max|R|): fp32 SIMT bit-exact vs the
+sequential fmaf oracle and <= 1e-4 vs double; TF32 / BF16 <= 5e-3 vs double on the operands
+the device consumed (bf16-rounded for BF16, reading Z16; fp32 for TF32, reading Z17).
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import synth  # noqa: E402
+from oracle import costs, gbfs as ogbfs, gemm as og, hw, space  # noqa: E402
+from oracle.rng import SplitMix64  # noqa: E402
+from oracle.space import Spec  # noqa: E402
+from paper_1909_10616_b200 import tiletune as tt  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def host_inputs(M, N, K, bf16=False, row0=0):
+    A = synth.uniform_f32(synth.SEED_A, M, K, row0=row0)
+    B = synth.uniform_f32(synth.SEED_B, K, N)
+    if bf16:
+        A = synth.bf16_bits_to_f32(synth.to_bf16_bits(A))
+        B = synth.bf16_bits_to_f32(synth.to_bf16_bits(B))
+    return A, B
+
+
+def to_dev(X, bf16=False):
+    t = torch.from_numpy(np.ascontiguousarray(X)).to(DEV)
+    return t.to(torch.bfloat16) if bf16 else t
+
+
+def run(fam, cfg, A, B):
+    bf16 = fam == tt.FAM_BF16_UMMA
+    Ad, Bd = to_dev(A, bf16), to_dev(B, bf16)
+    C = torch.full((A.shape[0], B.shape[1]), float("nan"), device=DEV)
+    tt.gemm(Ad, Bd, C, fam, cfg)
+    torch.cuda.synchronize()
+    return C.cpu().numpy()
+
+
+# ------------------------------------------------------------------ K4 generator
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_generator_bit_exact(dtype):
+    n, idx0 = 1 << 20, 12345
+    t = torch.empty(n, device=DEV, dtype=torch.float32 if dtype == "f32" else torch.bfloat16)
+    tt.fill_uniform(t, seed=2, idx0=idx0)
+    torch.cuda.synchronize()
+    ref = synth.uniform_f32(2, 1, n + idx0)[0, idx0:]
+    if dtype == "f32":
+        assert np.array_equal(t.cpu().numpy(), ref)
+    else:
+        got = t.cpu().view(torch.int16).numpy().view(np.uint16)
+        assert np.array_equal(got, synth.to_bf16_bits(ref))
+
+
+# ------------------------------------------------------------------ K1 fp32 SIMT
+def _random_feasible(sp, n, seed):
+    allst = [s for s in space.enumerate_configs(sp) if space.legitimate(sp, s)]
+    r = SplitMix64(seed)
+    return [allst[i] for i in r.sample_indices(len(allst), n)]
+
+
+@pytest.mark.parametrize("dims,n", [((64, 64, 64), 50), ((256, 256, 256), 20), ((256, 128, 64), 20)])
+def test_simt_random_configs_bit_exact(dims, n):
+    # S:533 acceptance 3: 50 random legitimate configs at 64^3, 20 at 256^3 (+ a non-square shape)
+    m, k, nn = dims
+    sp = Spec(m, k, nn, family=hw.FAM_F32_SIMT)
+    A, B = host_inputs(m, nn, k)
+    ref32 = og.gemm_fmaf(A, B)
+    R = og.gemm_f64(A, B)
+    for s in _random_feasible(sp, n, seed=m + k + nn):
+        C = run(tt.FAM_F32_SIMT, s, A, B)
+        assert np.array_equal(C, ref32), s
+        assert og.normwise_error(C, R) <= 1e-4
+
+
+def test_simt_s0_identity_ones_degenerate():
+    B = synth.uniform_f32(2, 128, 96)
+    I = np.eye(128, dtype=np.float32)
+    for s in [((128, 1, 1, 1), (128, 1), (96, 1, 1, 1)),        # the paper's untiled s0
+              ((2, 2, 8, 4), (16, 8), (3, 2, 4, 4))]:
+        assert np.array_equal(run(1, s, I, B), B)                  # pin 1
+    ones = run(1, ((2, 2, 8, 4), (16, 8), (2, 1, 4, 4)), np.ones((128, 128), np.float32),
+               np.ones((128, 32), np.float32))
+    assert (ones == 128).all()                                     # pin 4
+    # degenerate shapes: single row / column / k
+    for (M, N, K), s in [((1, 64, 32), ((1, 1, 1, 1), (4, 8), (4, 2, 8, 1))),
+                         ((64, 1, 16), ((8, 1, 8, 1), (1, 16), (1, 1, 1, 1))),
+                         ((32, 32, 1), ((2, 2, 8, 1), (1, 1), (2, 2, 4, 2)))]:
+        A, B = host_inputs(M, N, K)
+        assert np.array_equal(run(1, s, A, B), og.gemm_fmaf(A, B)), (M, N, K)
+
+
+def test_simt_large_sampled_rows():
+    # full size of the C2/C3 workloads: sampled rows against the oracle, one launch config
+    M = N = K = 2048
+    A, B = host_inputs(M, N, K)
+    s = ((16, 2, 8, 8), (256, 8), (16, 4, 4, 8))
+    C = run(1, s, A, B)
+    rows = np.array([0, 1, 127, 128, 1023, 2047])
+    R = og.gemm_f64_rows(A, B, rows)
+    assert og.normwise_error(C[rows], R) <= 1e-4
+    assert np.array_equal(C[rows], og.gemm_fmaf(A[rows], B))
+
+
+# ------------------------------------------------------------------ K2/K3 tcgen05
+@pytest.mark.parametrize("fam", [tt.FAM_BF16_UMMA, tt.FAM_TF32_UMMA])
+def test_umma_every_feasible_config_512(fam):
+    m = 512
+    sp = Spec(m, m, m, family=fam)
+    bf16 = fam == tt.FAM_BF16_UMMA
+    A, B = host_inputs(m, m, m, bf16=bf16)
+    R = og.gemm_f64(A, B)
+    bad = []
+    for s in space.enumerate_configs(sp):
+        if not space.legitimate(sp, s):
+            continue
+        C = run(fam, s, A, B)
+        err = og.normwise_error(C, R)
+        if not err <= 5e-3:
+            bad.append((s, err))
+    assert not bad, bad[:5]
+
+
+def test_umma_non_square_and_identity():
+    # (M, N, K) = (512, 256, 1024): several tiles on each axis, K loop of many stages
+    M, N, K = 512, 256, 1024
+    A, B = host_inputs(M, N, K, bf16=True)
+    R = og.gemm_f64(A, B)
+    for s in [((4, 1, 1, 128), (16, 64), (2, 1, 1, 128)), ((1, 2, 2, 128), (8, 128), (1, 1, 2, 128)),
+              ((2, 2, 1, 128), (64, 16), (8, 1, 1, 32)), ((4, 1, 1, 128), (4, 256), (16, 1, 1, 16))]:
+        assert og.normwise_error(run(3, s, A, B), R) <= 5e-3, s
+    I = np.eye(256, dtype=np.float32)
+    Bq = synth.bf16_bits_to_f32(synth.to_bf16_bits(synth.uniform_f32(2, 256, 256)))
+    assert np.array_equal(run(3, ((2, 1, 1, 128), (4, 64), (1, 1, 1, 256)), I, Bq), Bq)      # pin 1, exact
+    ones = run(3, ((1, 2, 1, 128), (16, 64), (2, 1, 1, 128)), np.ones((256, 1024), np.float32),
+               np.ones((1024, 256), np.float32))
+    assert (ones == 1024).all()                                                               # pin 4
+
+
+def test_tf32_rounding_mode_probe():
+    # reading Z17: which TF32 conversion does tcgen05 apply?  A = I, B with low mantissa bits
+    I = np.eye(128, dtype=np.float32)
+    B = synth.uniform_f32(2, 128, 128)
+    C = run(2, ((1, 1, 1, 128), (4, 32), (1, 1, 1, 128)), I, B)
+    bits = B.view(np.uint32)
+    trunc = (bits & np.uint32(0xFFFFE000)).view(np.float32)
+    rna = ((bits + np.uint32(0x1000)) & np.uint32(0xFFFFE000)).view(np.float32)
+    mode = "exact" if np.array_equal(C, B) else ("trunc" if np.array_equal(C, trunc) else
+                                                  ("rna" if np.array_equal(C, rna) else "other"))
+    print("TF32 operand conversion:", mode)
+    assert mode in ("trunc", "rna", "exact")
+
+
+def test_bf16_4096_sampled():
+    M = N = K = 4096
+    A, B = host_inputs(M, N, K, bf16=True)
+    rows = np.array([0, 129, 2048, 4095])
+    R = og.gemm_f64_rows(A, B, rows)
+    for s in [hw.default_s0(Spec(M, K, N, family=3)), ((16, 1, 2, 128), (64, 64), (16, 1, 1, 256)),
+              ((8, 2, 2, 128), (64, 64), (16, 1, 1, 256)), ((16, 2, 1, 128), (32, 128), (32, 1, 1, 128))]:
+        C = run(3, s, A, B)
+        assert og.normwise_error(C[rows], R) <= 5e-3, s
+        ii = np.array([5, 1000, 3000, 4095])
+        jj = np.array([4095, 17, 2222, 0])
+        assert og.normwise_error(C[ii, jj], og.gemm_f64_entries(A, B, ii, jj)) <= 5e-3
+
+
+# ------------------------------------------------------------------ evaluator and search
+def test_measure_and_errors():
+    ctx = tt.Context(0)
+    sp = tt.make_space(512, 512, 512, family=1)
+    smp = ctx.measure(sp, ((4, 2, 8, 8), (64, 8), (4, 4, 4, 8)))
+    assert smp.cost_s > 0 and smp.repeats == 10 and smp.min_s <= smp.cost_s and smp.number >= 1
+    assert smp.number * smp.cost_s >= 4e-4
+    with pytest.raises(tt.TileTuneError) as e:
+        ctx.measure(sp, ((4, 2, 8, 8), (64, 8), (4, 4, 4, 4)))
+    assert e.value.status == tt.E_ILLEGITIMATE
+    with pytest.raises(tt.TileTuneError) as e:
+        ctx.measure(sp, ((1, 1, 1, 512), (512, 1), (512, 1, 1, 1)))
+    assert e.value.status == tt.E_INFEASIBLE
+    cut = ctx.measure(sp, space.initial_state(Spec(512, 512, 512)), tt.measure_opts(cut_s=1e-6))
+    assert cut.slow_cut == 1 and cut.repeats == 1
+    fl = ctx.measure(sp, ((4, 2, 8, 8), (64, 8), (4, 4, 4, 8)), tt.measure_opts(l2_flush=1, repeats=3))
+    assert fl.number == 1 and fl.repeats == 3
+    ctx.close()
+
+
+class _Raw:
+    """Expose a raw device pointer to torch (CUDA array interface) without copying."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (ptr, False), "version": 3}
+
+
+def test_ctx_operands_are_the_recipe():
+    ctx = tt.Context(0, input_seed=1)
+    a, b, c = ctx.operands(64, 32, 16, tt.FAM_BF16_UMMA)
+    torch.cuda.synchronize()
+    A = torch.as_tensor(_Raw(a, (64, 16), "<i2"), device=DEV).cpu().numpy().view(np.uint16)
+    B = torch.as_tensor(_Raw(b, (16, 32), "<i2"), device=DEV).cpu().numpy().view(np.uint16)
+    assert np.array_equal(A, synth.to_bf16_bits(synth.uniform_f32(1, 64, 16)))
+    assert np.array_equal(B, synth.to_bf16_bits(synth.uniform_f32(2, 16, 32)))
+    ctx.close()
+
+
+def test_gemm_host_matches_device():
+    ctx = tt.Context(0)
+    M, N, K = 256, 256, 512
+    A, B = host_inputs(M, N, K)
+    Ah, Bh = torch.from_numpy(A).pin_memory(), torch.from_numpy(B).pin_memory()
+    Ch = torch.empty(M, N).pin_memory()
+    s = ((2, 2, 8, 8), (64, 8), (2, 4, 4, 8))
+    ctx.gemm_host(Ah, Bh, Ch, 1, s)
+    assert np.array_equal(Ch.numpy(), og.gemm_fmaf(A, B))
+    ctx.close()
+
+
+def test_gbfs_device_search_replay_parity():
+    # live G-BFS on the SIMT space of 512^3; replaying its (state -> cost) table through the
+    # oracle reproduces the identical sequence of evaluated states (O8 "live-GPU parity by replay")
+    ctx = tt.Context(0)
+    res = tt.gbfs_search(512, 512, 512, 120, tt.search_opts(family=1, seed=3), ctx=ctx)
+    ctx.close()
+    assert res.evals == 120 and res.best_cost < res.trace[0]["cost"]
+    table = {r["state"]: r["cost"] for r in res.trace}
+    sp = Spec(512, 512, 512, family=1)
+    o = ogbfs.gbfs(sp, lambda states: [table[s] for s in states], budget=120, rho=5, seed=3)
+    assert [r.state for r in o.trace] == [r["state"] for r in res.trace]
+    assert res.frac_raw == 120 / 484000
+
+
+def test_na2c_device_search():
+    ctx = tt.Context(0)
+    res = tt.na2c_search(512, 512, 512, 64, tt.search_opts(family=1, seed=1), ctx=ctx)
+    ctx.close()
+    assert res.evals == 64 and res.best_cost < res.trace[0]["cost"]
+    states = [r["state"] for r in res.trace]
+    assert len(set(states)) == 64
+
+
+def test_bf16_exhaustive_vs_gbfs_4096():
+    # every feasible BF16 config at 4096^3 measured once; G-BFS at <= 1% of the raw space must
+    # land within 5% of the exhaustive best (reading O10 machine-relative pin)
+    ctx = tt.Context(0)
+    sp = tt.make_space(4096, 4096, 4096, family=3)
+    cfgs, _ = tt.enumerate_feasible(sp)
+    mo = tt.measure_opts(repeats=5)
+    best = min(ctx.measure(sp, s, mo).cost_s for s in cfgs)
+    res = tt.gbfs_search(4096, 4096, 4096, 100, tt.search_opts(family=3, seed=0, measure={"repeats": 5}), ctx=ctx)
+    ctx.close()
+    assert res.frac_raw <= 0.01
+    assert res.best_cost <= best * 1.05, (res.best_cost, best)

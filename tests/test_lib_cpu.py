@@ -1,0 +1,240 @@
+"""CPU parity of the C-ABI library (libtiletune.so) against the oracle: configuration space,
+J_hw tables, G-BFS / N-A2C traversal under deterministic cost tables, ABI surface.  No GPU."""
+import math
+import os
+import re
+
+import pytest
+
+from oracle import costs, gbfs as ogbfs, hw, na2c as ona2c, space
+from oracle.rng import SplitMix64
+from oracle.space import Spec
+from paper_1909_10616_b200 import tiletune as tt
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def lib_space(sp: Spec):
+    # oracle Spec is (m, k, n); the ABI takes (M, N, K)
+    return tt.make_space(sp.m, sp.n, sp.k, sp.dm, sp.dk, sp.dn, sp.family)
+
+
+def test_abi_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "tiletune.h")).read()
+    declared = set(re.findall(r"\b(tt_[a-z0-9_]+)\s*\(", hdr)) - {"tt_cost_fn", "tt_batch_eval_fn"}
+    assert len(declared) >= 20
+    for name in sorted(declared):
+        assert hasattr(tt.lib, name), name
+    assert set(tt.EXPORTS) == declared
+    assert tt.lib.tt_version() == 1
+
+
+@pytest.mark.parametrize("dims,d,fam", [((512, 512, 512), (4, 2, 4), 0), ((1024, 1024, 1024), (4, 2, 4), 0),
+                                        ((2048, 2048, 2048), (4, 2, 4), 0), ((64, 64, 64), (4, 2, 4), 1),
+                                        ((12, 18, 30), (2, 3, 2), 0), ((256, 128, 512), (4, 2, 4), 1),
+                                        ((4096, 4096, 4096), (4, 2, 4), 3), ((2048, 2048, 2048), (4, 2, 4), 2),
+                                        ((1024, 8192, 8192), (4, 2, 4), 3), ((16, 16, 16), (1, 1, 1), 0)])
+def test_counts_match_oracle(dims, d, fam):
+    sp = Spec(*dims, *d, family=fam)
+    raw, feas = tt.count_configs(lib_space(sp), feasible=True)
+    assert raw == space.count_configs(sp)
+    if raw <= 600000:
+        assert feas == sum(1 for s in space.enumerate_configs(sp) if space.legitimate(sp, s))
+
+
+def test_overflow_reported():
+    p47 = 614889782588491410          # primorial 47#: 15 distinct primes -> 4^15 per axis at d = 4
+    sp = tt.make_space(p47, p47, p47, 4, 4, 4)
+    with pytest.raises(tt.TileTuneError) as e:
+        tt.count_configs(sp)
+    assert e.value.status == tt.E_OVERFLOW
+
+
+def test_enumeration_rank_legitimacy_neighbors_64():
+    sp = Spec(64, 64, 64)
+    ls = lib_space(sp)
+    ora = list(space.enumerate_configs(sp))
+    lib = tt.enumerate_configs(ls)
+    assert lib == ora                                        # bit-exact order (reading O4)
+    for r in range(0, len(ora), 211):
+        assert tt.rank(ls, ora[r]) == r and tt.unrank(ls, r) == ora[r]
+    for s in ora[::7]:
+        assert tt.neighbors(ls, s) == space.neighbors(sp, s)
+    assert tt.is_legitimate(ls, ((64, 1, 1, 1), (64, 1), (64, 1, 1, 1))) == (True, True)
+    assert tt.is_legitimate(ls, ((32, 1, 1, 1), (64, 1), (64, 1, 1, 1)))[0] is False
+    with pytest.raises(tt.TileTuneError) as e:
+        tt.rank(ls, ((32, 1, 1, 1), (64, 1), (64, 1, 1, 1)))
+    assert e.value.status == tt.E_ILLEGITIMATE
+
+
+def test_step_matches_oracle():
+    sp = Spec(1024, 1024, 1024)
+    ls = lib_space(sp)
+    s0 = space.initial_state(sp)
+    for (a, i, j) in space.actions(sp):
+        o = space.step(s0, (a, i, j))
+        o = o if (o is not None and space.legitimate(sp, o)) else None
+        assert tt.step(ls, s0, a, i, j) == o
+
+
+@pytest.mark.parametrize("dims,fam", [((512, 512, 512), 1), ((4096, 4096, 4096), 3), ((2048, 2048, 2048), 2),
+                                      ((512, 512, 512), 3)])
+def test_feasible_sets_match_oracle(dims, fam):
+    sp = Spec(*dims, family=fam)
+    cfgs, ranks = tt.enumerate_feasible(lib_space(sp))
+    ora = [(r, s) for r, s in enumerate(space.enumerate_configs(sp)) if hw.j_hw(sp, s)]
+    assert ranks == [r for r, _ in ora]
+    assert cfgs == [s for _, s in ora]
+
+
+def test_feasible_neighbors_match_oracle():
+    sp = Spec(4096, 4096, 4096, family=3)
+    ls = lib_space(sp)
+    for s in [s for s in space.enumerate_configs(sp) if hw.j_hw(sp, s)]:
+        assert tt.neighbors(ls, s) == space.neighbors(sp, s)
+    sp = Spec(512, 512, 512, family=1)
+    ls = lib_space(sp)
+    allst = list(space.enumerate_configs(sp))
+    for s in allst[::97]:
+        if space.legitimate(sp, s):
+            assert tt.neighbors(ls, s) == space.neighbors(sp, s)
+
+
+def _trace_key(rows):
+    return [(r["eval_index"], r["state"], r["cost"], r["best"]) for r in rows]
+
+
+def _oracle_key(res):
+    return [(r.eval_index, r.state, r.cost, r.best) for r in res.trace]
+
+
+@pytest.mark.parametrize("width", [1, 8])
+def test_gbfs_trace_parity_tables(width):
+    # reading O8: library trace == oracle trace byte-for-byte under T1 / T2, seeds 0-9
+    sp = Spec(64, 64, 64)
+    t1 = costs.table(sp, costs.t1_cost)
+    t2 = costs.table(sp, lambda s: costs.t2_cost(sp, s))
+    for tab in (t1, t2):
+        for seed in range(10):
+            o = ogbfs.gbfs(sp, ogbfs.table_source(sp, tab), budget=988, rho=5, seed=seed, width=width)
+            lres = tt.gbfs_search(64, 64, 64, 988, tt.search_opts(seed=seed, width=width, rho=5), table=tab)
+            assert _trace_key(lres.trace) == _oracle_key(o), (seed, width)
+            assert lres.best == o.best_state and lres.best_cost == o.best_cost
+            assert lres.evals == o.evals and lres.space_raw == 49392
+
+
+def test_gbfs_callback_and_completeness():
+    sp = Spec(16, 16, 16, 2, 2, 2)
+    tg = ((1.0, 3.0), (2.0, 2.0), (3.0, 1.0))
+    fn = lambda s: costs.t1_cost(s, targets=tg)
+    res = tt.gbfs_search(16, 16, 16, 0, tt.search_opts(dm=2, dk=2, dn=2, rho=6, seed=4), cost=fn)
+    assert res.evals == 125 and res.best_cost == ogbfs.brute_force(sp, fn)[0]
+    o = ogbfs.gbfs(sp, ogbfs.fn_source(fn), rho=6, seed=4)
+    assert _trace_key(res.trace) == _oracle_key(o)
+
+
+def test_gbfs_non_square_parity():
+    # (M, N, K) = (256, 64, 128): paper order (m, k, n) = (256, 128, 64)
+    sp = Spec(256, 128, 64)
+    tab = costs.table(sp, lambda s: costs.t2_cost(sp, s, seed_t=3))
+    o = ogbfs.gbfs(sp, ogbfs.table_source(sp, tab), budget=500, rho=5, seed=11)
+    lres = tt.gbfs_search(256, 64, 128, 500, tt.search_opts(seed=11), table=tab)
+    assert _trace_key(lres.trace) == _oracle_key(o)
+
+
+def test_gbfs_feasible_family_parity():
+    # family tables restrict g(s): parity on the SIMT space of 512^3 with a T2 table
+    sp = Spec(512, 512, 512, family=1)
+    tab = costs.table(sp, lambda s: costs.t2_cost(sp, s))
+    for seed in (0, 1):
+        o = ogbfs.gbfs(sp, ogbfs.table_source(sp, tab), budget=484, rho=5, seed=seed)
+        lres = tt.gbfs_search(512, 512, 512, 484, tt.search_opts(family=1, seed=seed), table=tab)
+        assert _trace_key(lres.trace) == _oracle_key(o)
+        assert lres.space_feasible == 130438
+
+
+def test_gbfs_bad_s0():
+    with pytest.raises(tt.TileTuneError) as e:
+        tt.gbfs_search(64, 64, 64, 10, tt.search_opts(has_s0=1, s0=tt.to_config(((32, 1, 1, 1), (64, 1), (64, 1, 1, 1)))),
+                       cost=lambda s: 1.0)
+    assert e.value.status == tt.E_INVAL
+
+
+def test_gbfs_batch_source_and_evaluator_failure():
+    sp = Spec(64, 64, 64)
+    seen = []
+
+    def batch(states):
+        seen.append(len(states))
+        return [costs.t1_cost(s) for s in states]
+
+    res = tt.gbfs_search(64, 64, 64, 300, tt.search_opts(seed=5, width=8), batch=batch)
+    o = ogbfs.gbfs(sp, ogbfs.fn_source(costs.t1_cost), budget=300, rho=5, seed=5, width=8)
+    assert _trace_key(res.trace) == _oracle_key(o)
+    assert max(seen) > 5                                     # W = 8 rounds expose > rho candidates
+
+    calls = []
+
+    def failing(states):
+        calls.append(1)
+        if len(calls) > 3:
+            raise RuntimeError("boom")
+        return [1.0] * len(states)
+
+    with pytest.raises(tt.TileTuneError) as e:
+        tt.gbfs_search(64, 64, 64, 300, tt.search_opts(seed=5), batch=failing)
+    assert e.value.status == tt.E_EVALUATOR
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+def test_na2c_eps0_trace_parity(seed):
+    # epsilon = 0: the policy is never consulted -> bit-exact traversal (reading O9)
+    sp = Spec(64, 64, 64)
+    tab = costs.table(sp, lambda s: costs.t2_cost(sp, s))
+    p = ona2c.Params(epsilon=0.0)
+    o = ona2c.na2c(sp, ogbfs.table_source(sp, tab), budget=300, params=p, seed=seed)
+    lres = tt.na2c_search(64, 64, 64, 300, tt.search_opts(seed=seed, epsilon=0.0), table=tab)
+    assert _trace_key(lres.trace) == _oracle_key(o)
+
+
+def test_na2c_eps0_small_batch_parity():
+    sp = Spec(64, 64, 64)
+    p = ona2c.Params(epsilon=0.0, batch=3, steps=2)
+    o = ona2c.na2c(sp, ogbfs.fn_source(costs.t1_cost), budget=150, params=p, seed=7)
+    lres = tt.na2c_search(64, 64, 64, 150, tt.search_opts(seed=7, epsilon=0.0, batch=3, steps_T=2),
+                          cost=costs.t1_cost)
+    assert _trace_key(lres.trace) == _oracle_key(o)
+
+
+def test_na2c_policy_properties():
+    # epsilon = 0.8 (policy consulted): exact trajectory is parity-unpinned; check the invariants
+    sp = Spec(64, 64, 64)
+    res = tt.na2c_search(64, 64, 64, 988, tt.search_opts(seed=3), cost=costs.t1_cost)
+    states = [r["state"] for r in res.trace]
+    assert len(states) == len(set(states)) == 988
+    bests = [r["best"] for r in res.trace]
+    assert all(x >= y for x, y in zip(bests, bests[1:]))
+    assert all(space.legitimate(sp, s) for s in states)
+    # S:536-style: beats random search on the T1 preset in most paired seeds
+    allst = list(space.enumerate_configs(sp))
+    wins = 0
+    for seed in range(10):
+        a = tt.na2c_search(64, 64, 64, 988, tt.search_opts(seed=seed), cost=costs.t1_cost).best_cost
+        pick = SplitMix64(1000 + seed).sample_indices(len(allst), 988)
+        wins += a <= min(costs.t1_cost(allst[i]) for i in pick)
+    assert wins >= 7
+
+
+def test_binding_simt_and_umma():
+    ls = tt.make_space(512, 512, 512, family=1)
+    b = tt.binding(ls, ((4, 2, 8, 8), (64, 8), (4, 4, 4, 8)))
+    assert (b.grid_x, b.grid_y, b.block_x, b.tile_m, b.tile_n, b.tile_k) == (4, 4, 256, 128, 128, 8)
+    assert b.smem_bytes == 2 * (128 + 128 + 8) * 8 * 4
+    ls = tt.make_space(4096, 4096, 4096, family=3)
+    b = tt.binding(ls, ((16, 2, 1, 128), (64, 64), (16, 1, 1, 256)))
+    assert b.cluster_x == 2 and b.tile_m == 256 and b.tile_n == 256 and b.stages >= 2
+    # idesc: F32 accum (bit 4), bf16 A/B (bits 7, 10), B MN-major (bit 16), N>>3 at 17, M>>4 at 24
+    assert b.idesc == (1 << 4) | (1 << 7) | (1 << 10) | (1 << 16) | ((256 >> 3) << 17) | ((256 >> 4) << 24)
+    with pytest.raises(tt.TileTuneError) as e:
+        tt.binding(ls, space.initial_state(Spec(4096, 4096, 4096)))
+    assert e.value.status == tt.E_INFEASIBLE
