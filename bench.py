@@ -1,0 +1,376 @@
+"""Benchmark of the hot path: G-BFS-tuned tiled GEMM on B200 (arXiv 1909.10616).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--workload NAME]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (one rank per GPU, NCCL)
+
+Metric (BASELINE.json): best-found GEMM TFLOP/s (and % of peak), tuning wall time and % of the
+configuration space explored.  Workload (default ``bf16_4096``, BASELINE configs[3]): C = A.B
+at 4096^3 with bf16 operands and fp32 accumulation/output on the tcgen05 family (K3).
+
+One run does, in order:
+ 1. the tuning pass (every SURVEY §8(a) row): space count / J_hw, G-BFS (Alg. 1, width W = 8,
+    rho = 5) with candidate batches measured by libtiletune's device evaluator -- sharded over
+    the ranks with an all_gather of the timings when N > 1 -- and the fraction explored;
+ 2. W untimed warm-up steps and K timed steps of the best-found GEMM, one launch per step on
+    each rank's row shard (rank r owns A rows [4096 r, 4096 (r+1)), B replicated, no collective
+    on the math path: weak scaling).  The L2 is flushed (256 MiB memset) before every step,
+    outside the CUDA-event pair that times the launch; barrier + synchronize on both sides;
+    the per-step time is the max over ranks.
+ 3. ``e2e``: the same GEMM through tt_gemm_host (pinned host A, B in; C out) per step;
+ 4. ``cpu_baseline``: the oracle's double GEMM (oracle/gemm_ref.c) on a bounded row sample.
+
+``--impl reference`` times the oracle alone (the reference arm of this tier), rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (M per rank, N, K, family, default budget)
+    "bf16_4096": (4096, 4096, 4096, 3, 64),
+    "tf32_2048": (2048, 2048, 2048, 2, 64),
+    "f32_2048": (2048, 2048, 2048, 1, 256),
+    "f32_512": (512, 512, 512, 1, 484),
+}
+FAMILY_DTYPE = {1: "f32", 2: "tf32", 3: "bf16"}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def fp32_fma_peak_tflops(sm_mhz: float) -> float:
+    # 148 SMs x 128 FP32 lanes x 2 flop/FMA x clock (guide unit counts)
+    return 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_oracle_sample(M, N, K, family, seconds: float = 12.0, max_rows: int = 4096):
+    """Time the oracle's double GEMM (oracle/gemm_ref.c, as it stands) on row blocks of the
+    workload until ``seconds`` of CPU work; returns (TFLOP/s, cores, sample description)."""
+    import numpy as np
+
+    import synth
+    from oracle import gemm as og
+    A = synth.uniform_f32(synth.SEED_A, M, K)
+    B = synth.uniform_f32(synth.SEED_B, K, N)
+    if family == 3:
+        A = synth.bf16_bits_to_f32(synth.to_bf16_bits(A))
+        B = synth.bf16_bits_to_f32(synth.to_bf16_bits(B))
+    A64, B64 = A.astype(np.float64), B.astype(np.float64)
+    og.gemm_f64_rows(A64, B64, [0])  # build + warm
+    rows_done, t_total, blk = 0, 0.0, 16
+    while t_total < seconds and rows_done < max_rows:
+        rows = np.arange(rows_done, min(rows_done + blk, M))
+        t0 = time.perf_counter()
+        og.gemm_f64_rows(A64, B64, rows)
+        t_total += time.perf_counter() - t0
+        rows_done += len(rows)
+        blk = min(blk * 2, 256)
+    flops = 2.0 * rows_done * N * K
+    cores = len(os.sched_getaffinity(0))
+    return flops / t_total / 1e12, cores, f"{rows_done} rows x {N} x {K} of the {M}x{N}x{K} product, " \
+                                          f"double triple loop, {t_total:.1f} s"
+
+
+def run_reference(args):
+    """Reference arm of this tier: the oracle as it stands on the host cores, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    import synth
+    from oracle import gemm as og
+    M, N, K, fam, _ = WORKLOADS[args.workload]
+    A = synth.uniform_f32(synth.SEED_A, M, K)
+    B = synth.uniform_f32(synth.SEED_B, K, N)
+    if fam == 3:
+        A = synth.bf16_bits_to_f32(synth.to_bf16_bits(A))
+        B = synth.bf16_bits_to_f32(synth.to_bf16_bits(B))
+    A64, B64 = A.astype(np.float64), B.astype(np.float64)
+    rows_per_step = args.ref_rows
+    times = []
+    for it in range(args.warmup + args.steps):
+        r0 = (it * rows_per_step) % M
+        rows = np.arange(r0, r0 + rows_per_step)
+        t0 = time.perf_counter()
+        og.gemm_f64_rows(A64, B64, rows)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+    ms = 1e3 * sum(times) / len(times)
+    flops = 2.0 * rows_per_step * N * K
+    value = flops / (ms * 1e-3) / 1e12
+    cores = len(os.sched_getaffinity(0))
+    sample = f"{rows_per_step} rows x {N} x {K} per step of the {M}x{N}x{K} product (double triple loop)"
+    print(json.dumps({
+        "impl": "reference", "metric": "best-found GEMM TFLOP/s", "value": value, "unit": "TFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": args.workload, "M": M, "N": N, "K": K},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="bf16_4096", choices=sorted(WORKLOADS))
+    ap.add_argument("--budget", type=int, default=None, help="G-BFS evaluation budget (distinct configs)")
+    ap.add_argument("--width", type=int, default=8)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--ref-rows", type=int, default=16)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", default=None, help="skip tuning and use this config (JSON triple)")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1909_10616_b200 import dist as tdist
+    from paper_1909_10616_b200 import tiletune as tt
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    Mr, N, K, fam, default_budget = WORKLOADS[args.workload]
+    M = Mr * world
+    budget = args.budget if args.budget is not None else default_budget
+    ctx = tt.Context(local, input_seed=1)
+    sp = tt.make_space(Mr, N, K, family=fam)
+    raw, feasible = tt.count_configs(sp, feasible=True)
+
+    # ---------------- 1. tuning pass (G-BFS, candidates sharded over ranks) ----------------
+    if args.config:
+        best = tuple(tuple(v) for v in json.loads(args.config))
+        tune = None
+    else:
+        measure_one, observe = tdist.device_measure(ctx, sp)
+        ev = tdist.TrackingEvaluator(measure_one, observe, device=dev if world > 1 else None)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        res = tt.gbfs_search(Mr, N, K, budget, tt.search_opts(family=fam, seed=args.seed, width=args.width), batch=ev)
+        tune_wall = tdist.max_over_ranks(time.perf_counter() - t0, dev)
+        best = res.best
+        tune = {"algorithm": "G-BFS (Alg. 1, width %d, rho 5)" % args.width, "budget": budget, "evals": res.evals,
+                "space_raw": raw, "space_feasible": feasible, "frac_raw": res.frac_raw,
+                "frac_feasible": res.frac_feasible, "tuning_wall_s": tune_wall, "best_config": best,
+                "best_cost_us": res.best_cost * 1e6, "s0_cost_us": res.trace[0]["cost"] * 1e6,
+                "local_evals": ev.local_evals}
+    info = tt.binding(sp, best)
+
+    # ---------------- 2. timed steps of the best-found GEMM on this rank's row shard ----------
+    bf16 = fam == 3
+    r0, r1 = tdist.row_shard(M, world, rank)
+    A = torch.empty(Mr, K, device=dev, dtype=torch.bfloat16 if bf16 else torch.float32)
+    B = torch.empty(K, N, device=dev, dtype=A.dtype)
+    C = torch.empty(Mr, N, device=dev, dtype=torch.float32)
+    tt.fill_uniform(A, seed=1, idx0=r0 * K)        # global row indices: shards == rows of the full A
+    tt.fill_uniform(B, seed=2)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for _ in range(args.warmup):
+        flush.fill_(1)
+        tt.gemm(A, B, C, fam, best)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)                           # L2 flush between steps (outside the events)
+        starts[i].record(stream)
+        tt.gemm(A, B, C, fam, best)
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    per = [s.elapsed_time(e) for s, e in zip(starts, ends)]       # ms, launching stream
+    ms_local = sum(per) / len(per)
+    ms = tdist.max_over_ranks(ms_local, dev)
+    flops_rank = 2.0 * Mr * N * K
+    value = world * flops_rank / (ms * 1e-3) / 1e12                 # whole-job TFLOP/s
+
+    # spot-check the timed output against the oracle on sampled entries (untimed)
+    import numpy as np
+
+    import synth
+    from oracle import gemm as og
+    ii = np.array([0, Mr // 3, Mr - 1])
+    jj = np.array([N - 1, N // 2, 0])
+    Ah = synth.uniform_f32(1, 3, K, row0=0)
+    Arows = np.stack([synth.uniform_f32(1, 1, K, row0=r0 + int(i))[0] for i in ii])
+    Bh = synth.uniform_f32(2, K, N)
+    if bf16:
+        Arows = synth.bf16_bits_to_f32(synth.to_bf16_bits(Arows))
+        Bh = synth.bf16_bits_to_f32(synth.to_bf16_bits(Bh))
+    ref = np.array([float(np.dot(Arows[t].astype(np.float64), Bh[:, jj[t]].astype(np.float64))) for t in range(3)])
+    got = C.cpu().numpy()[ii, jj]
+    spot_err = float(np.max(np.abs(got - ref)) / max(1e-30, np.max(np.abs(ref))))
+    del Ah
+
+    # ---------------- 3. e2e through tt_gemm_host (pinned host buffers) -----------------------
+    Ah_t = A.cpu().pin_memory()
+    Bh_t = B.cpu().pin_memory()
+    Ch_t = torch.empty(Mr, N, dtype=torch.float32).pin_memory()
+    ctx.gemm_host(Ah_t, Bh_t, Ch_t, fam, best)       # warm (allocates staging)
+    e2e_steps = min(args.steps, 5)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ctx.gemm_host(Ah_t, Bh_t, Ch_t, fam, best)
+    e2e_s = tdist.max_over_ranks((time.perf_counter() - t0) / e2e_steps, dev)
+    e2e_val = world * flops_rank / e2e_s / 1e12
+    h2d = Ah_t.numel() * Ah_t.element_size() + Bh_t.numel() * Bh_t.element_size()
+    d2h = Ch_t.numel() * 4
+
+    # ---------------- 4. roofline + cpu baseline (rank 0) --------------------------------------
+    peaks, peak_src = load_peaks()
+    if fam == 3:
+        peak = peaks["bf16_tflops"]
+        peak_note = f"bf16 dense, burst, {peak_src} (MEASURED_PEAKS.json)"
+        bound = "tensor"
+    elif fam == 2:
+        peak = peaks["bf16_tflops"] * 0.5
+        peak_note = f"tf32 = bf16 burst x 0.5 (nominal 1.1/2.25 ratio), {peak_src}"
+        bound = "tensor"
+    else:
+        smx = clocks.get("sm_max_mhz") or 1965.0
+        peak = fp32_fma_peak_tflops(smx)
+        peak_note = f"fp32 FFMA: 148 SM x 128 lanes x 2 x {smx:.0f} MHz (DESIGN.md §6)"
+        bound = "alu"
+    achieved = flops_rank / (ms_local * 1e-3) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tr = json.load(f)
+        if tr.get("config") == [list(v) for v in best]:
+            traffic = tr.get("dram_bytes_per_launch")
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, sample = cpu_oracle_sample(Mr, N, K, fam, seconds=args.cpu_seconds)
+        cpu = {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": "best-found GEMM TFLOP/s", "value": value, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": FAMILY_DTYPE[fam], "data": "synthetic",
+            "config": {"workload": args.workload, "M_per_rank": Mr, "M_total": M, "N": N, "K": K,
+                       "family": {1: "f32_simt", 2: "tf32_umma", 3: "bf16_umma"}[fam],
+                       "parallelism": f"row-partitioned x{world}, candidate sharding x{world}",
+                       "l2": "flushed (256 MiB memset) before every timed launch",
+                       "best_config": {"m": list(best[0]), "k": list(best[1]), "n": list(best[2])},
+                       "launch": {"grid": info.grid_x, "cluster": info.cluster_x, "tile": [info.tile_m, info.tile_n,
+                                  info.tile_k], "stages": info.stages, "smem": info.smem_bytes}},
+            "tuning": tune,
+            "pct_of_peak": 100.0 * achieved / peak,
+            "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_note,
+                         "algorithmic": f"2*M*N*K = {flops_rank:.4g} flop per launch"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "path": "tt_gemm_host (pinned host A,B -> device -> C host)"},
+            "gpu_launches": args.steps,
+            "clocks": clocks,
+            "spot_check_err": spot_err,
+            "per_step_ms": {"min": min(per), "median": statistics.median(per), "max": max(per)},
+        }
+        print(json.dumps(line))
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

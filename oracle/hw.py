@@ -86,7 +86,9 @@ def j_hw(spec, s) -> bool:
         if n3 % 16 != 0 or not (16 <= n3 <= 256):
             return False
         nb = n3 // m1                      # B columns per CTA per MMA (cta_group::2 splits N)
-        if nb * elem < 32:                 # smallest MN-major swizzle atom is 32 B
+        # smallest MN-major B swizzle atom: 32 B for bf16; MN-major tf32 exists only in the
+        # 128B-swizzle-with-32B-atoms layout, so a CTA's B columns must span 128 B
+        if nb * elem < (128 if fam == FAM_TF32_UMMA else 32):
             return False
         if m2 * n2 * n3 > UMMA_MAX_TMEM_COLS:
             return False

@@ -34,6 +34,8 @@ struct UmmaArgs {
   int stages, acc_bufs, acc_cols;   // acc_cols = m2 n2 n3 (columns per accumulator buffer)
   int tmem_cols;
   int swz_a, swz_b;                 // swizzle bytes: 32 | 64 | 128
+  int a_layout, b_layout;           // descriptor layout codes (SW128 2, SW64 4, SW32 6, SW128_BASE32B 1)
+  int sbo_b;                        // B stride between K core-matrix groups (bytes)
   int a_chunk_bytes;                // bytes of one A K-chunk (rows x swz_a)
   int b_cw;                         // B columns per TMA box (swz_b / elem)
   int nb;                           // B columns per CTA per atom = n3 / cta_group
@@ -105,10 +107,11 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint32_t bar
   }
 }
 
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, int swz) {
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, int layout_code) {
   // tcgen05 shared-memory matrix descriptor: start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46),
-  // version 1 [46,48), base offset 0, layout [61,64): SW128 = 2, SW64 = 4, SW32 = 6
-  const uint64_t layout = swz == 128 ? 2ull : (swz == 64 ? 4ull : 6ull);
+  // version 1 [46,48), base offset 0, layout [61,64): SW128 = 2, SW64 = 4, SW32 = 6,
+  // SW128 with 32-byte atoms (the only MN-major tf32 layout) = 1
+  const uint64_t layout = (uint64_t)layout_code;
   return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (layout << 61);
 }
@@ -265,7 +268,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
       const int ksteps = p.bk / UK;
       const int bboxes = p.nb / p.b_cw;
       const uint32_t sbo_a = 8u * p.swz_a;
-      const uint32_t lbo_b = (uint32_t)(p.bk * p.swz_b), sbo_b = 8u * p.swz_b;
+      const uint32_t lbo_b = (uint32_t)(p.bk * p.swz_b), sbo_b = (uint32_t)p.sbo_b;
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         mbar_wait(tempty0 + 8u * acc, aphase ^ 1u);
         tc_fence_after();
@@ -279,10 +282,10 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             const uint32_t kbytes = (uint32_t)(ks * UK * ELEM);
             const uint32_t a_off = (kbytes / p.swz_a) * p.a_chunk_bytes + (kbytes % p.swz_a);
             for (int mi = 0; mi < p.m2; ++mi) {
-              const uint64_t ad = smem_desc(sa + a_off + (uint32_t)(mi * 128 * p.swz_a), 16u, sbo_a, p.swz_a);
+              const uint64_t ad = smem_desc(sa + a_off + (uint32_t)(mi * 128 * p.swz_a), 16u, sbo_a, p.a_layout);
               for (int ni = 0; ni < p.n2; ++ni) {
                 const uint64_t bd = smem_desc(sb + (uint32_t)(ni * bboxes) * lbo_b + (uint32_t)(ks * UK * p.swz_b),
-                                              lbo_b, sbo_b, p.swz_b);
+                                              lbo_b, sbo_b, p.b_layout);
                 umma<KIND, CG>(dbase + (uint32_t)((mi * p.n2 + ni) * p.n3), ad, bd, p.idesc,
                                (kb | ks) != 0 ? 1u : 0u);
               }
@@ -365,6 +368,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn(std::string* err) {
 }
 
 CUtensorMapSwizzle swz_enum(int s) {
+  if (s == -128) return CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;   // 128B swizzle, 32B atoms (tf32 MN-major)
   return s == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : (s == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
 }
 
@@ -426,6 +430,16 @@ void plan_of(const Space& sp, const State& s, Plan* pl) {
   a.swz_a = std::min(a.bk * elem, 128);
   a.swz_b = std::min(a.nb * elem, 128);
   a.b_cw = a.swz_b / elem;
+  auto code = [](int swz) { return swz == 128 ? 2 : (swz == 64 ? 4 : 6); };
+  a.a_layout = code(a.swz_a);
+  if (kind == 1) {
+    // MN-major tf32: 128B swizzle with 32B atoms (4 K-rows per core-matrix group)
+    a.b_layout = 1;
+    a.sbo_b = 4 * 128;
+  } else {
+    a.b_layout = code(a.swz_b);
+    a.sbo_b = 8 * a.swz_b;
+  }
   a.a_chunk_bytes = a.m2 * 128 * a.swz_a;
   a.a_stage_bytes = a.m2 * 128 * a.bk * elem;
   a.stage_bytes = (int)umma_stage_bytes(fam, s);
@@ -518,7 +532,7 @@ tt_status umma_launch(const Space& sp, const State& s, const void* A, const void
                 (uint32_t)(pl.a.m2 * 128), pl.a.swz_a, err))
     return TT_E_CUDA;
   if (!make_map(&mb, pl.kind, B, (uint64_t)pl.a.N, (uint64_t)pl.a.K, (uint32_t)pl.a.b_cw, (uint32_t)pl.a.bk,
-                pl.a.swz_b, err))
+                pl.a.b_layout == 1 ? -128 : pl.a.swz_b, err))
     return TT_E_CUDA;
   if (pl.kind == 0) {
     return pl.cg == 1 ? launch_t<0, 1>(pl, ma, mb, C, stream, err) : launch_t<0, 2>(pl, ma, mb, C, stream, err);

@@ -158,7 +158,8 @@ bool Space::j_hw(const State& s) const {
     if (n1 != 1 || (n2 != 1 && n2 != 2)) return false;
     if (n3 % 16 != 0 || n3 < 16 || n3 > 256) return false;
     const int64_t nb = n3 / m1;
-    if (nb * umma_elem(family) < 32) return false;
+    // MN-major B atom: >= 32 B (bf16); tf32 MN-major only as 128B swizzle with 32B atoms
+    if (nb * umma_elem(family) < (family == TT_FAM_TF32_UMMA ? 128 : 32)) return false;
     if (m2 * n2 * n3 > 512) return false;
     if (k1 % umma_k(family) != 0 || k1 > 256) return false;
     if ((n3 & (n3 - 1)) || (k1 & (k1 - 1))) return false;   // swizzle widths 32/64/128 B

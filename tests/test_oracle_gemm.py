@@ -136,7 +136,9 @@ def test_jhw_umma_boundaries():
     assert not space.legitimate(sp, ((32, 1, 1, 128), (512, 8), (32, 1, 1, 128)))  # BK % 16
     tf = Spec(2048, 2048, 2048, family=hw.FAM_TF32_UMMA)
     assert space.legitimate(tf, hw.default_s0(tf))
-    assert space.legitimate(tf, ((16, 1, 1, 128), (256, 8), (128, 1, 1, 16)))
+    assert space.legitimate(tf, ((16, 1, 1, 128), (256, 8), (64, 1, 1, 32)))
+    assert not space.legitimate(tf, ((16, 1, 1, 128), (256, 8), (128, 1, 1, 16)))  # tf32 MN-major needs 128 B
+    assert not space.legitimate(tf, ((8, 2, 1, 128), (256, 8), (64, 1, 1, 32)))    # 2-CTA: 16 cols = 64 B
     assert not space.legitimate(tf, ((16, 1, 1, 128), (2048, 1), (128, 1, 1, 16)))
 
 
