@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -26,6 +27,8 @@
 namespace tt {
 
 namespace {
+
+constexpr int kEpiBytes = 32768;   // epilogue staging (the J_hw reserve)
 
 struct UmmaArgs {
   int64_t M, N, K;
@@ -42,6 +45,7 @@ struct UmmaArgs {
   int a_stage_bytes, stage_bytes;   // A part, total per stage (A + padded B)
   uint32_t idesc;
   uint32_t tx_bytes;                // bytes landing per stage per CTA
+  int dbg;                          // experiment knobs (env TT_UMMA_DBG); 0 in production
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -65,10 +69,30 @@ __device__ __forceinline__ uint64_t globaltimer() {
 }
 // Watchdog: a pipeline that has not advanced for 10 s traps (a launch error the host reports)
 // instead of hanging the GPU.
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  if (mbar_try(bar, parity)) return;
+__device__ __forceinline__ bool mbar_try_nohint(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}" : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}" : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+  return ok != 0;
+}
+__device__ int g_wait_mode;   // experiment knob: 0 try_wait+hint, 1 try_wait, 2 test_wait spin
+__device__ __forceinline__ bool mbar_poll(uint32_t bar, uint32_t parity, int mode) {
+  return mode == 0 ? mbar_try(bar, parity) : (mode == 1 ? mbar_try_nohint(bar, parity) : mbar_test(bar, parity));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int mode = 0) {
+  if (mbar_poll(bar, parity, mode)) return;
   const uint64_t t0 = globaltimer();
-  while (!mbar_try(bar, parity)) {
+  while (!mbar_poll(bar, parity, mode)) {
     if (globaltimer() - t0 > 10000000000ull) __trap();
   }
 }
@@ -83,6 +107,23 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar, uint32_t cta) 
       "{\n\t.reg .b32 ra;\n\t"
       "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
       "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(bar), "r"(cta) : "memory");
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+               ::"l"(map), "r"(x), "r"(y), "r"(src) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+  return pred != 0;
 }
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -177,21 +218,24 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 // ---------------------------------------------------------------- the kernel
 template <int KIND, int CG>
 __global__ void __launch_bounds__(256, 1)
-k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, float* __restrict__ C,
+k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+       const __grid_constant__ CUtensorMap tmC, float* __restrict__ C,
        const UmmaArgs p) {
   constexpr int ELEM = KIND == 0 ? 2 : 4;
   constexpr int UK = KIND == 0 ? 16 : 8;     // UMMA_K
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)p.stages * p.stage_bytes);
+  const uint32_t epi_base = sbase + (uint32_t)p.stages * p.stage_bytes;   // 4 warps x 2 x 4 KB staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)p.stages * p.stage_bytes + kEpiBytes);
   const uint32_t full0 = smem_u32(bars);
   const uint32_t empty0 = full0 + 8u * p.stages;
   const uint32_t tfull0 = empty0 + 8u * p.stages;
   const uint32_t tempty0 = tfull0 + 16u;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * p.stages + 4);
 
-  const int warp = threadIdx.x >> 5;
+  // warp index made provably warp-uniform so role loops run on the uniform datapath
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
   const bool leader = rank == 0;
@@ -199,6 +243,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmC) : "memory");
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
@@ -231,44 +276,58 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
   const int rows_cta = p.m2 * 128;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ===== TMA producer =====
-      int stage = 0;
-      uint32_t phase = 0;
-      const int kchunks = p.bk * ELEM / p.swz_a;
-      const int bboxes = p.nb / p.b_cw;
-      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
-        const int tm = tile % p.m0, tn = tile / p.m0;
-        const int row = tm * (CG * rows_cta) + (int)rank * rows_cta;
-        const int colt = tn * (p.n2 * p.n3) + (int)rank * p.nb;
-        for (int kb = 0; kb < p.k0; ++kb) {
-          mbar_wait(empty0 + 8u * stage, phase ^ 1u);
-          const uint32_t fb = full0 + 8u * stage;
+    // ===== TMA producer: the whole warp walks the ring, one elected lane issues =====
+    int stage = 0;
+    uint32_t phase = 0;
+    const int kchunks = p.bk * ELEM / p.swz_a;
+    const int bboxes = p.nb / p.b_cw;
+    const uint32_t bbox_bytes = (uint32_t)(p.bk * p.swz_b);
+    const int a_kstep = p.swz_a / ELEM;
+    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+      const int tm = tile % p.m0, tn = tile / p.m0;
+      const int row = tm * (CG * rows_cta) + (int)rank * rows_cta;
+      const int colt = tn * (p.n2 * p.n3) + (int)rank * p.nb;
+      for (int kb = 0; kb < p.k0; ++kb) {
+        mbar_wait(empty0 + 8u * stage, phase ^ 1u);
+        const uint32_t fb = full0 + 8u * stage;
+        if (elect_one()) {
           if (leader) mbar_arrive_expect_tx(fb, p.tx_bytes * CG);
           const uint32_t sa = sbase + (uint32_t)stage * p.stage_bytes;
           const uint32_t sb = sa + p.a_stage_bytes;
           for (int kc = 0; kc < kchunks; ++kc)
-            tma_load_2d<CG>(&tmA, fb, sa + kc * p.a_chunk_bytes, kb * p.bk + kc * (p.swz_a / ELEM), row);
+            tma_load_2d<CG>(&tmA, fb, sa + kc * p.a_chunk_bytes, kb * p.bk + kc * a_kstep, row);
           for (int ni = 0; ni < p.n2; ++ni)
             for (int c = 0; c < bboxes; ++c)
-              tma_load_2d<CG>(&tmB, fb, sb + (uint32_t)((ni * bboxes + c) * p.bk * p.swz_b),
-                              colt + ni * p.n3 + c * p.b_cw, kb * p.bk);
+              tma_load_2d<CG>(&tmB, fb, sb + (uint32_t)(ni * bboxes + c) * bbox_bytes, colt + ni * p.n3 + c * p.b_cw,
+                              kb * p.bk);
           if (CG == 2 && !leader) mbar_arrive_cluster(fb, 0);
-          if (++stage == p.stages) { stage = 0; phase ^= 1u; }
         }
+        __syncwarp();
+        if (++stage == p.stages) { stage = 0; phase ^= 1u; }
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
-      // ===== MMA issuer =====
+    if (leader) {
+      // ===== MMA issuer: warp-uniform loop, one elected lane issues tcgen05.mma =====
+      // Descriptor high words are loop invariant; only the 14-bit start-address field of the
+      // low word moves (smem addresses < 256 KB, so the add never carries out of the field).
+      const int ksteps = p.bk / UK;
+      const int bboxes = p.nb / p.b_cw;
+      const uint32_t lbo_b = (uint32_t)(p.bk * p.swz_b);
+      const uint32_t a_hi = (uint32_t)(smem_desc(0, 16u, 8u * (uint32_t)p.swz_a, p.a_layout) >> 32);
+      const uint32_t b_hi = (uint32_t)(smem_desc(0, lbo_b, (uint32_t)p.sbo_b, p.b_layout) >> 32);
+      const uint32_t a_lbo = 1u << 16;
+      const uint32_t b_lbo = ((lbo_b >> 4) & 0x3FFFu) << 16;
+      const uint32_t a_atom16 = (uint32_t)(128 * p.swz_a) >> 4;         // next M atom
+      const uint32_t b_atom16 = ((uint32_t)bboxes * lbo_b) >> 4;          // next N atom
+      const uint32_t b_kstep16 = (uint32_t)(UK * p.swz_b) >> 4;           // next UMMA_K rows
+      const uint32_t a_chunk16 = (uint32_t)p.a_chunk_bytes >> 4;
+      const uint32_t a_kstep16 = (uint32_t)(UK * ELEM) >> 4;              // 32 B
+      const uint32_t a_inrow16 = (uint32_t)p.swz_a >> 4;
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t aphase = 0;
-      const int ksteps = p.bk / UK;
-      const int bboxes = p.nb / p.b_cw;
-      const uint32_t sbo_a = 8u * p.swz_a;
-      const uint32_t lbo_b = (uint32_t)(p.bk * p.swz_b), sbo_b = (uint32_t)p.sbo_b;
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         mbar_wait(tempty0 + 8u * acc, aphase ^ 1u);
         tc_fence_after();
@@ -276,55 +335,74 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
         for (int kb = 0; kb < p.k0; ++kb) {
           mbar_wait(full0 + 8u * stage, phase);
           tc_fence_after();
-          const uint32_t sa = sbase + (uint32_t)stage * p.stage_bytes;
-          const uint32_t sb = sa + p.a_stage_bytes;
+          const uint32_t sa16 = (sbase + (uint32_t)stage * p.stage_bytes) >> 4;
+          const uint32_t sb16 = sa16 + ((uint32_t)p.a_stage_bytes >> 4);
+          uint32_t a_in = 0, a_ch = 0;
           for (int ks = 0; ks < ksteps; ++ks) {
-            const uint32_t kbytes = (uint32_t)(ks * UK * ELEM);
-            const uint32_t a_off = (kbytes / p.swz_a) * p.a_chunk_bytes + (kbytes % p.swz_a);
+            const uint32_t acc_flag = (kb | ks) != 0 ? 1u : 0u;
             for (int mi = 0; mi < p.m2; ++mi) {
-              const uint64_t ad = smem_desc(sa + a_off + (uint32_t)(mi * 128 * p.swz_a), 16u, sbo_a, p.a_layout);
+              const uint64_t ad = ((uint64_t)a_hi << 32) | (uint64_t)((sa16 + a_ch + a_in + mi * a_atom16) | a_lbo);
               for (int ni = 0; ni < p.n2; ++ni) {
-                const uint64_t bd = smem_desc(sb + (uint32_t)(ni * bboxes) * lbo_b + (uint32_t)(ks * UK * p.swz_b),
-                                              lbo_b, sbo_b, p.b_layout);
-                umma<KIND, CG>(dbase + (uint32_t)((mi * p.n2 + ni) * p.n3), ad, bd, p.idesc,
-                               (kb | ks) != 0 ? 1u : 0u);
+                const uint64_t bd = ((uint64_t)b_hi << 32) |
+                                    (uint64_t)((sb16 + ni * b_atom16 + ks * b_kstep16) | b_lbo);
+                if (elect_one()) umma<KIND, CG>(dbase + (uint32_t)((mi * p.n2 + ni) * p.n3), ad, bd, p.idesc, acc_flag);
               }
             }
+            a_in += a_kstep16;
+            if (a_in == a_inrow16) { a_in = 0; a_ch += a_chunk16; }
           }
-          umma_commit<CG>(empty0 + 8u * stage);           // frees the smem slot when MMAs finish
+          if (elect_one()) umma_commit<CG>(empty0 + 8u * stage);   // frees the smem slot when MMAs finish
+          __syncwarp();
           if (++stage == p.stages) { stage = 0; phase ^= 1u; }
         }
-        umma_commit<CG>(tfull0 + 8u * acc);                // accumulator ready for the epilogue
+        if (elect_one()) umma_commit<CG>(tfull0 + 8u * acc);     // accumulator ready for the epilogue
+        __syncwarp();
         if (++acc == p.acc_bufs) { acc = 0; aphase ^= 1u; }
       }
     }
   } else if (warp >= 4) {
-    // ===== epilogue: TMEM -> registers -> global =====
-    const int q = warp & 3;                                // TMEM lanes [32q, 32q+32)
+    // ===== epilogue: TMEM -> registers -> swizzled smem box -> TMA bulk store =====
+    // Each warp owns TMEM lanes [32q, 32q+32) (= 32 output rows) and two 4 KB staging boxes
+    // (32 rows x 32 fp32, 128B-swizzled like the C tensor map) used alternately; one lane
+    // issues cp.async.bulk.tensor stores, so C leaves the SM as full 128 B lines.
+    const int q = warp & 3;
+    const uint32_t stage0 = epi_base + (uint32_t)q * 8192u;
     int acc = 0;
     uint32_t aphase = 0;
+    int sbuf = 0;
     float v[32];
     for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
       const int tm = tile % p.m0, tn = tile / p.m0;
       mbar_wait(tfull0 + 8u * acc, aphase);
       tc_fence_after();
-      const int64_t row_cta = (int64_t)tm * (CG * rows_cta) + (int64_t)rank * rows_cta;
+      const int row_cta = tm * (CG * rows_cta) + (int)rank * rows_cta;
       for (int mi = 0; mi < p.m2; ++mi) {
-        const int64_t row = row_cta + mi * 128 + q * 32 + lane;
-        float* crow = C + row * p.N + (int64_t)tn * (p.n2 * p.n3);
+        const int row0 = row_cta + mi * 128 + q * 32;
         for (int ni = 0; ni < p.n2; ++ni) {
           const uint32_t tcol = (uint32_t)(acc * p.acc_cols + (mi * p.n2 + ni) * p.n3);
           const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + tcol;
+          const int col0 = tn * (p.n2 * p.n3) + ni * p.n3;
           int c0 = 0;
           for (; c0 + 32 <= p.n3; c0 += 32) {
             tmem_ld32(taddr + (uint32_t)c0, v);
-            float4* dst = reinterpret_cast<float4*>(crow + ni * p.n3 + c0);
+            const uint32_t buf = stage0 + (uint32_t)sbuf * 4096u;
+            if (lane == 0) bulk_wait_read<1>();            // the store that used `buf` has read it
+            __syncwarp();
+            const uint32_t rowp = buf + (uint32_t)lane * 128u;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            for (int j = 0; j < 8; ++j)
+              st_shared_v4(rowp + (uint32_t)((j ^ (lane & 7)) << 4), v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmC, buf, col0 + c0, row0);
+              bulk_commit();
+            }
+            sbuf ^= 1;
           }
-          if (c0 < p.n3) {                                 // n3 = 16 (UMMA_N multiple of 16)
+          if (c0 < p.n3) {                                 // n3 = 16: direct 16-column stores
             tmem_ld16(taddr + (uint32_t)c0, v);
-            float4* dst = reinterpret_cast<float4*>(crow + ni * p.n3 + c0);
+            float4* dst = reinterpret_cast<float4*>(C + (int64_t)(row0 + lane) * p.N + col0 + c0);
 #pragma unroll
             for (int j = 0; j < 4; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           }
@@ -332,12 +410,14 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
+      if (lane == 0) {                                     // TMEM drained: MMA may reuse `acc`
         if (CG == 1 || leader) mbar_arrive(tempty0 + 8u * acc);
         else mbar_arrive_cluster(tempty0 + 8u * acc, 0);
       }
       if (++acc == p.acc_bufs) { acc = 0; aphase ^= 1u; }
     }
+    if (lane == 0) bulk_wait_all();                         // stores done before smem is released
+    __syncwarp();
   }
 
   __syncwarp();                                            // reconverge role warps
@@ -460,11 +540,14 @@ void plan_of(const Space& sp, const State& s, Plan* pl) {
   const int tiles = a.m0 * a.n0;
   const int max_clusters = num_sms() / m1;
   pl->grid = std::min(tiles, max_clusters) * m1;
-  pl->smem = a.stages * a.stage_bytes + 1024 /*align*/ + 8 * (2 * a.stages + 4) + 16;
+  pl->smem = a.stages * a.stage_bytes + kEpiBytes + 1024 /*align*/ + 8 * (2 * a.stages + 4) + 16;
+  static const int dbg = getenv("TT_UMMA_DBG") ? atoi(getenv("TT_UMMA_DBG")) : 0;
+  a.dbg = dbg;
 }
 
 template <int KIND, int CG>
-tt_status launch_t(const Plan& pl, const CUtensorMap& ma, const CUtensorMap& mb, float* C, cudaStream_t stream,
+tt_status launch_t(const Plan& pl, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, float* C,
+                   cudaStream_t stream,
                    std::string* err) {
   auto fn = &k_umma<KIND, CG>;
   static bool attr = false;
@@ -486,7 +569,7 @@ tt_status launch_t(const Plan& pl, const CUtensorMap& ma, const CUtensorMap& mb,
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  if (!cuda_ok(cudaLaunchKernelEx(&cfg, fn, ma, mb, C, pl.a), err, "k_umma launch")) return TT_E_CUDA;
+  if (!cuda_ok(cudaLaunchKernelEx(&cfg, fn, ma, mb, mc, C, pl.a), err, "k_umma launch")) return TT_E_CUDA;
   return TT_OK;
 }
 
@@ -527,17 +610,19 @@ tt_status umma_launch(const Space& sp, const State& s, const void* A, const void
     *err = "UMMA family needs row pitches that are multiples of 16 bytes";
     return TT_E_UNSUPPORTED;
   }
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mc;
   if (!make_map(&ma, pl.kind, A, (uint64_t)pl.a.K, (uint64_t)pl.a.M, (uint32_t)(pl.a.swz_a / elem),
                 (uint32_t)(pl.a.m2 * 128), pl.a.swz_a, err))
     return TT_E_CUDA;
   if (!make_map(&mb, pl.kind, B, (uint64_t)pl.a.N, (uint64_t)pl.a.K, (uint32_t)pl.a.b_cw, (uint32_t)pl.a.bk,
                 pl.a.b_layout == 1 ? -128 : pl.a.swz_b, err))
     return TT_E_CUDA;
+  // C: fp32 [M][N], 32 x 32 boxes, 128B swizzle (matches the epilogue staging layout)
+  if (!make_map(&mc, 1, C, (uint64_t)pl.a.N, (uint64_t)pl.a.M, 32u, 32u, 128, err)) return TT_E_CUDA;
   if (pl.kind == 0) {
-    return pl.cg == 1 ? launch_t<0, 1>(pl, ma, mb, C, stream, err) : launch_t<0, 2>(pl, ma, mb, C, stream, err);
+    return pl.cg == 1 ? launch_t<0, 1>(pl, ma, mb, mc, C, stream, err) : launch_t<0, 2>(pl, ma, mb, mc, C, stream, err);
   }
-  return pl.cg == 1 ? launch_t<1, 1>(pl, ma, mb, C, stream, err) : launch_t<1, 2>(pl, ma, mb, C, stream, err);
+  return pl.cg == 1 ? launch_t<1, 1>(pl, ma, mb, mc, C, stream, err) : launch_t<1, 2>(pl, ma, mb, mc, C, stream, err);
 }
 
 }  // namespace tt
