@@ -45,7 +45,6 @@ struct UmmaArgs {
   int a_stage_bytes, stage_bytes;   // A part, total per stage (A + padded B)
   uint32_t idesc;
   uint32_t tx_bytes;                // bytes landing per stage per CTA
-  int dbg;                          // experiment knobs (env TT_UMMA_DBG); 0 in production
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -69,30 +68,10 @@ __device__ __forceinline__ uint64_t globaltimer() {
 }
 // Watchdog: a pipeline that has not advanced for 10 s traps (a launch error the host reports)
 // instead of hanging the GPU.
-__device__ __forceinline__ bool mbar_try_nohint(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred P;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
-      "selp.b32 %0, 1, 0, P;\n\t}" : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred P;\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
-      "selp.b32 %0, 1, 0, P;\n\t}" : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
-  return ok != 0;
-}
-__device__ int g_wait_mode;   // experiment knob: 0 try_wait+hint, 1 try_wait, 2 test_wait spin
-__device__ __forceinline__ bool mbar_poll(uint32_t bar, uint32_t parity, int mode) {
-  return mode == 0 ? mbar_try(bar, parity) : (mode == 1 ? mbar_try_nohint(bar, parity) : mbar_test(bar, parity));
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int mode = 0) {
-  if (mbar_poll(bar, parity, mode)) return;
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  if (mbar_try(bar, parity)) return;
   const uint64_t t0 = globaltimer();
-  while (!mbar_poll(bar, parity, mode)) {
+  while (!mbar_try(bar, parity)) {
     if (globaltimer() - t0 > 10000000000ull) __trap();
   }
 }
@@ -215,6 +194,69 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+struct MmaCtx {
+  uint32_t sbase, full0, empty0, tfull0, tempty0, tmem_base;
+  int cluster_id, num_clusters, num_tiles;
+};
+
+template <int KIND, int CG, int KS, int M2, int N2>
+__device__ __forceinline__ void mma_role(const UmmaArgs& p, const MmaCtx& c) {
+  constexpr int ELEM = KIND == 0 ? 2 : 4;
+  constexpr int UK = KIND == 0 ? 16 : 8;
+  // descriptor words: high halves are invariant; low halves = (start >> 4) | (LBO >> 4) << 16
+  const uint32_t lbo_b = (uint32_t)(p.bk * p.swz_b);
+  const uint64_t a_hi = smem_desc(0, 16u, 8u * (uint32_t)p.swz_a, p.a_layout) & 0xFFFFFFFF00000000ull;
+  const uint64_t b_hi = smem_desc(0, lbo_b, (uint32_t)p.sbo_b, p.b_layout) & 0xFFFFFFFF00000000ull;
+  const uint32_t a_lbo = 1u << 16;
+  const uint32_t b_lbo = ((lbo_b >> 4) & 0x3FFFu) << 16;
+  uint32_t a_off[KS][M2], b_off[KS][N2], d_off[M2][N2];
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    const uint32_t kbytes = (uint32_t)(ks * UK * ELEM);
+#pragma unroll
+    for (int mi = 0; mi < M2; ++mi)
+      a_off[ks][mi] = (((kbytes / p.swz_a) * p.a_chunk_bytes + kbytes % p.swz_a + mi * 128 * p.swz_a) >> 4) | a_lbo;
+#pragma unroll
+    for (int ni = 0; ni < N2; ++ni)
+      b_off[ks][ni] = (((uint32_t)(ni * (p.nb / p.b_cw)) * lbo_b + (uint32_t)(ks * UK * p.swz_b)) >> 4) | b_lbo;
+  }
+#pragma unroll
+  for (int mi = 0; mi < M2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < N2; ++ni) d_off[mi][ni] = (uint32_t)((mi * N2 + ni) * p.n3);
+  int stage = 0;
+  uint32_t phase = 0;
+  int acc = 0;
+  uint32_t aphase = 0;
+  for (int tile = c.cluster_id; tile < c.num_tiles; tile += c.num_clusters) {
+    mbar_wait(c.tempty0 + 8u * acc, aphase ^ 1u);
+    tc_fence_after();
+    const uint32_t dbase = c.tmem_base + (uint32_t)(acc * p.acc_cols);
+    for (int kb = 0; kb < p.k0; ++kb) {
+      mbar_wait(c.full0 + 8u * stage, phase);
+      tc_fence_after();
+      const uint32_t sa16 = (c.sbase + (uint32_t)stage * p.stage_bytes) >> 4;
+      const uint32_t sb16 = sa16 + ((uint32_t)p.a_stage_bytes >> 4);
+      if (elect_one()) {
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+          for (int mi = 0; mi < M2; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < N2; ++ni)
+              umma<KIND, CG>(dbase + d_off[mi][ni], a_hi | (uint64_t)(sa16 + a_off[ks][mi]),
+                             b_hi | (uint64_t)(sb16 + b_off[ks][ni]), p.idesc, (kb | ks) != 0 ? 1u : 0u);
+        umma_commit<CG>(c.empty0 + 8u * stage);              // frees the smem slot when MMAs finish
+      }
+      __syncwarp();
+      if (++stage == p.stages) { stage = 0; phase ^= 1u; }
+    }
+    if (elect_one()) umma_commit<CG>(c.tfull0 + 8u * acc);   // accumulator ready for the epilogue
+    __syncwarp();
+    if (++acc == p.acc_bufs) { acc = 0; aphase ^= 1u; }
+  }
+}
+
 // ---------------------------------------------------------------- the kernel
 template <int KIND, int CG>
 __global__ void __launch_bounds__(256, 1)
@@ -247,7 +289,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
-      mbar_init(full0 + 8u * s, CG);
+      mbar_init(full0 + 8u * s, 1);     // leader arms with both CTAs' bytes
       mbar_init(empty0 + 8u * s, 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -300,7 +342,6 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             for (int c = 0; c < bboxes; ++c)
               tma_load_2d<CG>(&tmB, fb, sb + (uint32_t)(ni * bboxes + c) * bbox_bytes, colt + ni * p.n3 + c * p.b_cw,
                               kb * p.bk);
-          if (CG == 2 && !leader) mbar_arrive_cluster(fb, 0);
         }
         __syncwarp();
         if (++stage == p.stages) { stage = 0; phase ^= 1u; }
@@ -308,56 +349,23 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     }
   } else if (warp == 1) {
     if (leader) {
-      // ===== MMA issuer: warp-uniform loop, one elected lane issues tcgen05.mma =====
-      // Descriptor high words are loop invariant; only the 14-bit start-address field of the
-      // low word moves (smem addresses < 256 KB, so the add never carries out of the field).
-      const int ksteps = p.bk / UK;
-      const int bboxes = p.nb / p.b_cw;
-      const uint32_t lbo_b = (uint32_t)(p.bk * p.swz_b);
-      const uint32_t a_hi = (uint32_t)(smem_desc(0, 16u, 8u * (uint32_t)p.swz_a, p.a_layout) >> 32);
-      const uint32_t b_hi = (uint32_t)(smem_desc(0, lbo_b, (uint32_t)p.sbo_b, p.b_layout) >> 32);
-      const uint32_t a_lbo = 1u << 16;
-      const uint32_t b_lbo = ((lbo_b >> 4) & 0x3FFFu) << 16;
-      const uint32_t a_atom16 = (uint32_t)(128 * p.swz_a) >> 4;         // next M atom
-      const uint32_t b_atom16 = ((uint32_t)bboxes * lbo_b) >> 4;          // next N atom
-      const uint32_t b_kstep16 = (uint32_t)(UK * p.swz_b) >> 4;           // next UMMA_K rows
-      const uint32_t a_chunk16 = (uint32_t)p.a_chunk_bytes >> 4;
-      const uint32_t a_kstep16 = (uint32_t)(UK * ELEM) >> 4;              // 32 B
-      const uint32_t a_inrow16 = (uint32_t)p.swz_a >> 4;
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t aphase = 0;
-      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
-        mbar_wait(tempty0 + 8u * acc, aphase ^ 1u);
-        tc_fence_after();
-        const uint32_t dbase = tmem_base + (uint32_t)(acc * p.acc_cols);
-        for (int kb = 0; kb < p.k0; ++kb) {
-          mbar_wait(full0 + 8u * stage, phase);
-          tc_fence_after();
-          const uint32_t sa16 = (sbase + (uint32_t)stage * p.stage_bytes) >> 4;
-          const uint32_t sb16 = sa16 + ((uint32_t)p.a_stage_bytes >> 4);
-          uint32_t a_in = 0, a_ch = 0;
-          for (int ks = 0; ks < ksteps; ++ks) {
-            const uint32_t acc_flag = (kb | ks) != 0 ? 1u : 0u;
-            for (int mi = 0; mi < p.m2; ++mi) {
-              const uint64_t ad = ((uint64_t)a_hi << 32) | (uint64_t)((sa16 + a_ch + a_in + mi * a_atom16) | a_lbo);
-              for (int ni = 0; ni < p.n2; ++ni) {
-                const uint64_t bd = ((uint64_t)b_hi << 32) |
-                                    (uint64_t)((sb16 + ni * b_atom16 + ks * b_kstep16) | b_lbo);
-                if (elect_one()) umma<KIND, CG>(dbase + (uint32_t)((mi * p.n2 + ni) * p.n3), ad, bd, p.idesc, acc_flag);
-              }
-            }
-            a_in += a_kstep16;
-            if (a_in == a_inrow16) { a_in = 0; a_ch += a_chunk16; }
-          }
-          if (elect_one()) umma_commit<CG>(empty0 + 8u * stage);   // frees the smem slot when MMAs finish
-          __syncwarp();
-          if (++stage == p.stages) { stage = 0; phase ^= 1u; }
-        }
-        if (elect_one()) umma_commit<CG>(tfull0 + 8u * acc);     // accumulator ready for the epilogue
-        __syncwarp();
-        if (++acc == p.acc_bufs) { acc = 0; aphase ^= 1u; }
+      // ===== MMA issuer: specialised on (k-steps per stage, M atoms, N atoms) so the per-stage
+      // MMA sequence is fully unrolled with loop-invariant descriptor words (issue stays far
+      // below the 64-128 cycles one MMA occupies the tensor pipe).
+      const int code = (p.bk / UK) * 4 + (p.m2 - 1) * 2 + (p.n2 - 1);
+      MmaCtx c{sbase, full0, empty0, tfull0, tempty0, tmem_base, cluster_id, num_clusters, num_tiles};
+      switch (code) {
+#define TT_MMA_CASE(KS, M2, N2) \
+  case KS * 4 + (M2 - 1) * 2 + (N2 - 1): mma_role<KIND, CG, KS, M2, N2>(p, c); break;
+#define TT_MMA_KS(KS) TT_MMA_CASE(KS, 1, 1) TT_MMA_CASE(KS, 1, 2) TT_MMA_CASE(KS, 2, 1) TT_MMA_CASE(KS, 2, 2)
+        TT_MMA_KS(1) TT_MMA_KS(2) TT_MMA_KS(4) TT_MMA_KS(8) TT_MMA_KS(16)
+#undef TT_MMA_KS
+#undef TT_MMA_CASE
+        case 32 * 4 + 0: if constexpr (KIND == 1) mma_role<KIND, CG, 32, 1, 1>(p, c); break;
+        case 32 * 4 + 1: if constexpr (KIND == 1) mma_role<KIND, CG, 32, 1, 2>(p, c); break;
+        case 32 * 4 + 2: if constexpr (KIND == 1) mma_role<KIND, CG, 32, 2, 1>(p, c); break;
+        case 32 * 4 + 3: if constexpr (KIND == 1) mma_role<KIND, CG, 32, 2, 2>(p, c); break;
+        default: __trap();
       }
     }
   } else if (warp >= 4) {
@@ -541,8 +549,6 @@ void plan_of(const Space& sp, const State& s, Plan* pl) {
   const int max_clusters = num_sms() / m1;
   pl->grid = std::min(tiles, max_clusters) * m1;
   pl->smem = a.stages * a.stage_bytes + kEpiBytes + 1024 /*align*/ + 8 * (2 * a.stages + 4) + 16;
-  static const int dbg = getenv("TT_UMMA_DBG") ? atoi(getenv("TT_UMMA_DBG")) : 0;
-  a.dbg = dbg;
 }
 
 template <int KIND, int CG>

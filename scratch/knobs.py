@@ -1,6 +1,7 @@
 import sys, os, subprocess
-cfgs = ["((16,2,1,128),(64,64),(16,1,1,256))", "((16,2,1,128),(32,128),(8,1,2,256))", "((32,1,1,128),(64,64),(16,1,1,256))", "((32,1,1,128),(64,64),(8,1,2,256))"]
-for dbg in [0, 2]:
+cfgs = ["((16,2,1,128),(64,64),(16,1,1,256))", "((16,2,1,128),(64,64),(8,1,2,256))", "((32,1,1,128),(64,64),(16,1,1,256))", "((32,1,1,128),(64,64),(8,1,2,256))", "((16,1,2,128),(64,64),(16,1,1,256))"]
+print("configs:", cfgs)
+for dbg in [int(x) for x in sys.argv[1:]] or [0, 1, 2, 3, 8, 10]:
     code = f"""
 import sys; sys.path.insert(0,'.')
 from paper_1909_10616_b200 import tiletune as tt
