@@ -30,7 +30,8 @@ struct SimtArgs {
   float* C;
   int64_t M, N, K;
   int m1, m2, n1, n2, bk, k0;
-  int a_vec;  // As base 16-byte aligned (float4 reads legal)
+  int bk_sh;  // log2(BK) if BK is a power of two, else -1
+  int bq_sh;  // log2(BN / 4) if a power of two, else -1
   int b_vec;  // B rows 16-byte aligned (16-byte cp.async legal)
 };
 
@@ -80,16 +81,30 @@ k1_simt(SimtArgs p) {
     float* bs = Bs + buf * BK * LDB;
     const int64_t kb = (int64_t)kt * BK;
     const int na = BM * BK;
-    for (int e = t; e < na; e += T) {
-      const int r = e / BK, c = e - (e / BK) * BK;
-      cp_async4(as + c * LDA + r, Ab + (int64_t)r * K + kb + c);
+    if (p.bk_sh >= 0) {                    // power-of-two BK: shifts instead of divisions
+      for (int e = t; e < na; e += T) {
+        const int r = e >> p.bk_sh, c = e & (BK - 1);
+        cp_async4(as + c * LDA + r, Ab + (int64_t)r * K + kb + c);
+      }
+    } else {
+      for (int e = t; e < na; e += T) {
+        const int r = e / BK, c = e - (e / BK) * BK;
+        cp_async4(as + c * LDA + r, Ab + (int64_t)r * K + kb + c);
+      }
     }
     if (p.b_vec) {
       const int q = BN >> 2;
       const int nb = BK * q;
-      for (int e = t; e < nb; e += T) {
-        const int r = e / q, c = (e - (e / q) * q) << 2;
-        cp_async16(bs + r * LDB + c, Bb + (kb + r) * N + c);
+      if (p.bq_sh >= 0) {
+        for (int e = t; e < nb; e += T) {
+          const int r = e >> p.bq_sh, c = (e & (q - 1)) << 2;
+          cp_async16(bs + r * LDB + c, Bb + (kb + r) * N + c);
+        }
+      } else {
+        for (int e = t; e < nb; e += T) {
+          const int r = e / q, c = (e - (e / q) * q) << 2;
+          cp_async16(bs + r * LDB + c, Bb + (kb + r) * N + c);
+        }
       }
     } else {
       const int nb = BK * BN;
@@ -100,11 +115,21 @@ k1_simt(SimtArgs p) {
     }
   };
 
+  // kVecA: TM, TN multiples of 4 => BN % 4 == 0 => the As base (2 BK LDB floats) is 16 B aligned
+  constexpr bool kVecA = (TM % 4 == 0) && (TN % 4 == 0);
+  constexpr bool kPair = (TN % 2 == 0);
   float acc[TM][TN];
+  float2 acc2[TM][kPair ? TN / 2 : 1];
 #pragma unroll
-  for (int i = 0; i < TM; ++i)
+  for (int i = 0; i < TM; ++i) {
+    if constexpr (kPair) {
 #pragma unroll
-    for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;
+      for (int j = 0; j < TN / 2; ++j) acc2[i][j] = make_float2(0.0f, 0.0f);
+    } else {
+#pragma unroll
+      for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;
+    }
+  }
 
   load(0, 0);
   cp_async_commit();
@@ -123,16 +148,11 @@ k1_simt(SimtArgs p) {
 #pragma unroll 2
     for (int kk = 0; kk < BK; ++kk) {
       float a[TM], b[TN];
-      if constexpr (TM % 4 == 0) {
-        if (p.a_vec) {
+      if constexpr (kVecA) {
 #pragma unroll
-          for (int i = 0; i < TM; i += 4) {
-            const float4 v = *reinterpret_cast<const float4*>(as + kk * LDA + i);
-            a[i] = v.x; a[i + 1] = v.y; a[i + 2] = v.z; a[i + 3] = v.w;
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < TM; ++i) a[i] = as[kk * LDA + i];
+        for (int i = 0; i < TM; i += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(as + kk * LDA + i);
+          a[i] = v.x; a[i + 1] = v.y; a[i + 2] = v.z; a[i + 3] = v.w;
         }
       } else {
 #pragma unroll
@@ -148,12 +168,32 @@ k1_simt(SimtArgs p) {
 #pragma unroll
         for (int j = 0; j < TN; ++j) b[j] = bs[kk * LDB + j];
       }
+      if constexpr (kPair) {
+        // FFMA2: two independent fused multiply-adds per instruction, each rounded once, so
+        // every output is still the same fmaf chain in ascending k as the scalar path.
 #pragma unroll
-      for (int i = 0; i < TM; ++i)
+        for (int i = 0; i < TM; ++i) {
+          const float2 ai = make_float2(a[i], a[i]);
 #pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+          for (int j = 0; j < TN / 2; ++j) acc2[i][j] = __ffma2_rn(ai, make_float2(b[2 * j], b[2 * j + 1]), acc2[i][j]);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+      }
     }
     __syncthreads();
+  }
+  if constexpr (kPair) {
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN / 2; ++j) {
+        acc[i][2 * j] = acc2[i][j].x;
+        acc[i][2 * j + 1] = acc2[i][j].y;
+      }
   }
 
   float* Cb = p.C + ((int64_t)blockIdx.y * BM + row0) * N + (int64_t)blockIdx.x * BN + col0;
@@ -261,7 +301,10 @@ tt_status simt_launch(const Space& sp, const State& s, const float* A, const flo
   a.bk = (int)s.f[1][1];
   a.k0 = (int)s.f[1][0];
   const int64_t LDB = li.tile_n + 4;
-  a.a_vec = ((2 * (int64_t)a.bk * LDB) % 4 == 0) ? 1 : 0;
+  (void)LDB;
+  auto lg = [](int64_t v) -> int { if (v <= 0 || (v & (v - 1))) return -1; int l = 0; while ((int64_t(1) << l) < v) ++l; return l; };
+  a.bk_sh = lg(a.bk);
+  a.bq_sh = (li.tile_n % 4 == 0) ? lg(li.tile_n / 4) : -1;
   a.b_vec = (li.tile_n % 4 == 0 && a.N % 4 == 0 && ((uintptr_t)B % 16) == 0) ? 1 : 0;
   dim3 grid((unsigned)li.grid_x, (unsigned)li.grid_y, 1);
   fn<<<grid, li.block_x, li.smem_bytes, stream>>>(a);
