@@ -1,0 +1,21 @@
+# small-shape runs of every kernel family for compute-sanitizer
+import sys
+sys.path.insert(0, '.')
+import torch
+from paper_1909_10616_b200 import tiletune as tt
+dev = torch.device('cuda:0')
+for fam, n, cfgs in [(1, 128, [((2, 2, 8, 4), (16, 8), (2, 2, 4, 8)), ((128, 1, 1, 1), (128, 1), (128, 1, 1, 1)), ((1, 4, 4, 8), (4, 32), (2, 2, 8, 4))]),
+                     (3, 512, [((4, 1, 1, 128), (8, 64), (4, 1, 1, 128)), ((1, 2, 2, 128), (8, 64), (2, 1, 1, 256)), ((2, 2, 1, 128), (32, 16), (16, 1, 1, 32))]),
+                     (2, 256, [((2, 1, 1, 128), (8, 32), (2, 1, 1, 128)), ((1, 2, 1, 128), (32, 8), (1, 1, 1, 256))])]:
+    dt = torch.bfloat16 if fam == 3 else torch.float32
+    A = torch.randn(n, n, device=dev).to(dt)
+    B = torch.randn(n, n, device=dev).to(dt)
+    C = torch.empty(n, n, device=dev)
+    for s in cfgs:
+        tt.gemm(A, B, C, fam, s)
+        torch.cuda.synchronize()
+        ref = A.float() @ B.float()
+        print(fam, s, float((C - ref).abs().max() / ref.abs().max()))
+ctx = tt.Context(0)
+res = tt.gbfs_search(128, 128, 128, 8, tt.search_opts(family=1, seed=0, measure={"repeats": 2}), ctx=ctx)
+print("search ok", res.evals)
