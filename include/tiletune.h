@@ -260,6 +260,13 @@ tt_status tt_na2c_search(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, uint64_t 
                          const tt_search_opts* opts, tt_result* out, tt_trace_row* trace,
                          uint64_t trace_cap);
 
+/* Random-search comparator ("configurations are randomly selected to be tested"):
+ * the first budget_evals states of a uniform random permutation (SplitMix64 partial Fisher-Yates
+ * with opts->seed) of the feasible set in rank order, measured in batches of opts->width.  Not the
+ * paper's method; the baseline the searches are compared against. */
+tt_status tt_random_search(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, uint64_t budget_evals,
+                           const tt_search_opts* opts, tt_result* out, tt_trace_row* trace, uint64_t trace_cap);
+
 #ifdef __cplusplus
 }
 #endif

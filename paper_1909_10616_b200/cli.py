@@ -1,0 +1,237 @@
+"""Command-line front end (SPEC S:440-526 subcommands; every step runs in libtiletune).
+
+    python -m paper_1909_10616_b200.cli count     --m 1024 --k 1024 --n 1024 [--dm 4 --dk 2 --dn 4] [--family bf16]
+    python -m paper_1909_10616_b200.cli enumerate --m 64 --k 64 --n 64 [--limit 20] [--feasible]
+    python -m paper_1909_10616_b200.cli bench     --m 4096 --k 4096 --n 4096 --family bf16 --config '{"m":[..],"k":[..],"n":[..]}'
+    python -m paper_1909_10616_b200.cli tune      --m 512 --k 512 --n 512 --family f32 --strategy gbfs --max-evals 484 --seeds 0,1 --out runs/t
+    python -m paper_1909_10616_b200.cli compare   --m 512 --k 512 --n 512 --family f32 --strategies gbfs,na2c,random --max-evals 484 --seeds 0-9 --out runs/c
+
+Problems are given in the paper's (m, k, n) order; C[m x n] = A[m x k] B[k x n].
+Configurations use the canonical text form {"m":[...],"k":[...],"n":[...]}, outer -> inner.
+``tune`` / ``compare`` write a CSV trace (one row per measured state) and a JSON summary
+with the box-plot statistics of the paper's Fig. 8(b) (min, Q1, median, mean, Q3, max over seeds,
+P:397).  Cost sources: ``--backend device`` (the B200 evaluator) or ``synthetic`` (S:172 landscape,
+for desk runs without a GPU).
+"""
+from __future__ import annotations
+
+import argparse
+import csv
+import json
+import math
+import os
+import statistics
+import sys
+import time
+from typing import List
+
+from . import tiletune as tt
+
+FAMILIES = {"none": tt.FAM_NONE, "f32": tt.FAM_F32_SIMT, "tf32": tt.FAM_TF32_UMMA, "bf16": tt.FAM_BF16_UMMA}
+
+
+def encode(s) -> str:
+    return '{"m":[%s],"k":[%s],"n":[%s]}' % tuple(",".join(str(v) for v in s[a]) for a in range(3))
+
+
+def decode(text: str, depths=(4, 2, 4)):
+    d = json.loads(text)
+    if not isinstance(d, dict) or set(d) != {"m", "k", "n"}:
+        raise ValueError("config must have keys m, k, n")
+    s = []
+    for key, dep in zip(("m", "k", "n"), depths):
+        v = d[key]
+        if not isinstance(v, list) or not all(isinstance(x, int) and not isinstance(x, bool) for x in v):
+            raise ValueError(f"non-integer entry in {key}")
+        if len(v) != dep:
+            raise ValueError(f"{key} has {len(v)} factors, depth is {dep}")
+        s.append(tuple(v))
+    return tuple(s)
+
+
+def parse_seeds(text: str) -> List[int]:
+    out = []
+    for part in text.split(","):
+        if "-" in part:
+            a, b = part.split("-")
+            out.extend(range(int(a), int(b) + 1))
+        elif part:
+            out.append(int(part))
+    return out
+
+
+def box(values):
+    xs = sorted(values)
+    n = len(xs)
+
+    def q(p):
+        if n == 1:
+            return xs[0]
+        pos = p * (n - 1)
+        lo = int(math.floor(pos))
+        hi = min(lo + 1, n - 1)
+        return xs[lo] + (xs[hi] - xs[lo]) * (pos - lo)
+
+    return {"min": xs[0], "q1": q(0.25), "median": q(0.5), "mean": sum(xs) / n, "q3": q(0.75), "max": xs[-1],
+            "n": n}
+
+
+def synthetic_cost(args):
+    """S:175 quadratic-in-log2 landscape with per-slot targets at half the log2 of each dim."""
+    dims = (args.m, args.k, args.n)
+    depths = (args.dm, args.dk, args.dn)
+    targets = [[math.log2(d) / dep for _ in range(dep)] for d, dep in zip(dims, depths)]
+
+    def f(s):
+        c = 1.0
+        for a in range(3):
+            for i, v in enumerate(s[a]):
+                c += (math.log2(v) - targets[a][i]) ** 2
+        return c
+    return f
+
+
+def _space(args):
+    return tt.make_space(args.m, args.n, args.k, args.dm, args.dk, args.dn, FAMILIES[args.family])
+
+
+def cmd_count(args):
+    raw, feas = tt.count_configs(_space(args), feasible=True)
+    print(raw if args.family == "none" else f"{raw} raw, {feas} feasible ({args.family})")
+
+
+def cmd_enumerate(args):
+    sp = _space(args)
+    if args.feasible:
+        cfgs, ranks = tt.enumerate_feasible(sp)
+        for r, s in list(zip(ranks, cfgs))[:args.limit]:
+            print(r, encode(s))
+    else:
+        for r, s in enumerate(tt.enumerate_configs(sp, 0, args.limit)):
+            print(r, encode(s))
+
+
+def cmd_bench(args):
+    sp = _space(args)
+    s = decode(args.config, (args.dm, args.dk, args.dn))
+    ctx = tt.Context(args.device)
+    smp = ctx.measure(sp, s, tt.measure_opts(repeats=args.repeats, warmup=args.warmup))
+    flops = 2.0 * args.m * args.n * args.k
+    print(json.dumps({"config": encode(s), "cost_s": smp.cost_s, "mean_s": smp.mean_s, "min_s": smp.min_s,
+                      "repeats": smp.repeats, "number": smp.number, "tflops": flops / smp.cost_s / 1e12}))
+
+
+def _run(strategy, args, seed, ctx):
+    opts = tt.search_opts(family=FAMILIES[args.family], dm=args.dm, dk=args.dk, dn=args.dn, seed=seed,
+                          rho=args.rho, width=args.width, steps_T=args.steps, epsilon=args.epsilon,
+                          batch=args.batch_size, gamma=args.gamma,
+                          budget_seconds=args.max_seconds or 0.0,
+                          measure={"repeats": args.repeats, "warmup": args.warmup})
+    if args.start_config:
+        opts.has_s0 = 1
+        opts.s0 = tt.to_config(decode(args.start_config, (args.dm, args.dk, args.dn)))
+    fn = {"gbfs": tt.gbfs_search, "na2c": tt.na2c_search, "random": tt.random_search}[strategy]
+    kw = {"ctx": ctx} if args.backend == "device" else {"cost": synthetic_cost(args)}
+    return fn(args.m, args.n, args.k, args.max_evals, opts, **kw)
+
+
+def _tune(args, strategies):
+    seeds = parse_seeds(args.seeds)
+    ctx = tt.Context(args.device) if args.backend == "device" else None
+    os.makedirs(os.path.dirname(os.path.abspath(args.out)) or ".", exist_ok=True)
+    rows, summary = [], {"problem": {"m": args.m, "k": args.k, "n": args.n, "d": [args.dm, args.dk, args.dn],
+                                     "family": args.family, "backend": args.backend},
+                         "seeds": seeds, "max_evals": args.max_evals, "strategies": {}}
+    flops = 2.0 * args.m * args.n * args.k
+    for strat in strategies:
+        bests, walls = [], []
+        for seed in seeds:
+            res = _run(strat, args, seed, ctx)
+            bests.append(res.best_cost)
+            walls.append(res.wall_s)
+            for r in res.trace:
+                rows.append([strat, seed, r["eval_index"], f"{r['t_wall_s']:.6f}", encode(r["state"]), repr(r["cost"]),
+                             repr(r["best"]), f"{(r['eval_index'] + 1) / res.space_raw:.9f}"])
+            print(f"{strat} seed {seed}: best {res.best_cost:.6g} after {res.evals} evals "
+                  f"({100 * res.frac_raw:.4f}% of {res.space_raw}, {res.wall_s:.1f} s) {encode(res.best)}", flush=True)
+        st = {"best_cost": box(bests), "wall_s": box(walls)}
+        if args.backend == "device":
+            st["best_tflops"] = box([flops / c / 1e12 for c in bests])
+        summary["strategies"][strat] = st
+    with open(args.out + ".csv", "w", newline="") as f:
+        w = csv.writer(f)
+        w.writerow(["strategy", "trial_seed", "eval_index", "wall_clock_s", "config", "cost_s", "best_so_far_s",
+                    "fraction_explored"])
+        w.writerows(rows)
+    with open(args.out + ".json", "w") as f:
+        json.dump(summary, f, indent=1)
+    print(json.dumps(summary["strategies"], indent=1))
+
+
+def cmd_tune(args):
+    _tune(args, [args.strategy])
+
+
+def cmd_compare(args):
+    strategies = [s for s in args.strategies.split(",") if s]
+    if len(strategies) < 2:
+        raise SystemExit("compare needs at least two strategies (S:502)")
+    _tune(args, strategies)
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(prog="tiletune")
+    sub = ap.add_subparsers(dest="cmd", required=True)
+
+    def common(p):
+        p.add_argument("--m", type=int, required=True)
+        p.add_argument("--k", type=int, required=True)
+        p.add_argument("--n", type=int, required=True)
+        p.add_argument("--dm", type=int, default=4)
+        p.add_argument("--dk", type=int, default=2)
+        p.add_argument("--dn", type=int, default=4)
+        p.add_argument("--family", choices=sorted(FAMILIES), default="none")
+        p.add_argument("--device", type=int, default=0)
+
+    p = sub.add_parser("count")
+    common(p)
+    p.set_defaults(fn=cmd_count)
+    p = sub.add_parser("enumerate")
+    common(p)
+    p.add_argument("--limit", type=int, default=20)
+    p.add_argument("--feasible", action="store_true")
+    p.set_defaults(fn=cmd_enumerate)
+    p = sub.add_parser("bench")
+    common(p)
+    p.add_argument("--config", required=True)
+    p.add_argument("--repeats", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=2)
+    p.set_defaults(fn=cmd_bench)
+    for name, fn in (("tune", cmd_tune), ("compare", cmd_compare)):
+        p = sub.add_parser(name)
+        common(p)
+        if name == "tune":
+            p.add_argument("--strategy", choices=["gbfs", "na2c", "random"], default="gbfs")
+        else:
+            p.add_argument("--strategies", default="gbfs,na2c,random")
+        p.add_argument("--backend", choices=["device", "synthetic"], default="device")
+        p.add_argument("--seeds", default="0")
+        p.add_argument("--max-evals", type=int, default=100)
+        p.add_argument("--max-seconds", type=float, default=0.0)
+        p.add_argument("--rho", type=int, default=5)
+        p.add_argument("--width", type=int, default=1)
+        p.add_argument("--steps", type=int, default=3)
+        p.add_argument("--epsilon", type=float, default=0.8)
+        p.add_argument("--batch-size", type=int, default=16)
+        p.add_argument("--gamma", type=float, default=0.9)
+        p.add_argument("--repeats", type=int, default=10)
+        p.add_argument("--warmup", type=int, default=2)
+        p.add_argument("--start-config", default=None)
+        p.add_argument("--out", default="runs/tune")
+        p.set_defaults(fn=fn)
+    args = ap.parse_args(argv)
+    args.fn(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -396,6 +396,13 @@ tt_status tt_gbfs_search(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, uint64_t 
   return run_search(gbfs_search, ctx, M, N, K, budget_evals, opts, out, trace, trace_cap);
 }
 
+tt_status tt_random_search(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, uint64_t budget_evals,
+                           const tt_search_opts* opts, tt_result* out, tt_trace_row* trace, uint64_t trace_cap) {
+  auto fn = [](const Space& sp, const State&, uint64_t budget, const tt_search_opts& o, const BatchCost& cost,
+               SearchOut* so, std::string* err) { return random_search(sp, budget, o, cost, so, err); };
+  return run_search(fn, ctx, M, N, K, budget_evals, opts, out, trace, trace_cap);
+}
+
 tt_status tt_na2c_search(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, uint64_t budget_evals,
                          const tt_search_opts* opts, tt_result* out, tt_trace_row* trace, uint64_t trace_cap) {
   return run_search(na2c_search, ctx, M, N, K, budget_evals, opts, out, trace, trace_cap);

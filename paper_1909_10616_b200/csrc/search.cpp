@@ -433,4 +433,66 @@ tt_status na2c_search(const Space& sp, const State& s0, uint64_t budget, const t
   return result;
 }
 
+// ------------------------------------------------------------------------------------------
+// Random search comparator: draw order = partial Fisher-Yates over the feasible
+// states in rank order with SplitMix64(seed); measured in batches of `width` in draw order.
+// ------------------------------------------------------------------------------------------
+tt_status random_search(const Space& sp, uint64_t budget, const tt_search_opts& o, const BatchCost& cost,
+                        SearchOut* out, std::string* err) {
+  std::vector<State> feas;
+  {
+    State s;
+    for (const Vec& vm : sp.lists[0])
+      for (const Vec& vk : sp.lists[1])
+        for (const Vec& vn : sp.lists[2]) {
+          s.f[0] = vm;
+          s.f[1] = vk;
+          s.f[2] = vn;
+          if (sp.j_hw(s)) feas.push_back(s);
+        }
+  }
+  const uint64_t L = feas.size();
+  if (L == 0) {
+    *err = "no feasible state";
+    return TT_E_INVAL;
+  }
+  if (budget == 0 || budget > L) budget = L;
+  const int width = o.width > 0 ? o.width : 1;
+  SplitMix64 rng(o.seed);
+  std::vector<uint64_t> idx(L);
+  for (uint64_t i = 0; i < L; ++i) idx[i] = i;
+  for (uint64_t t = 0; t < budget; ++t) {
+    const uint64_t j = t + rng.bounded(L - t);
+    std::swap(idx[t], idx[j]);
+  }
+  const double t0 = now_s();
+  uint64_t evals = 0;
+  out->best_cost = std::numeric_limits<double>::infinity();
+  std::vector<State> batch;
+  std::vector<double> costs;
+  tt_status result = TT_OK;
+  while (evals < budget) {
+    if (evals > 0 && o.budget_seconds > 0 && now_s() - t0 >= o.budget_seconds) break;
+    batch.clear();
+    for (uint64_t t = evals; t < budget && batch.size() < (size_t)width; ++t) batch.push_back(feas[idx[t]]);
+    costs.clear();
+    tt_status st = cost(batch, out->best_cost, &costs, err);
+    if (st != TT_OK) {
+      result = evals ? TT_E_EVALUATOR : (st == TT_E_CUDA ? TT_E_EVALUATOR : st);
+      break;
+    }
+    for (size_t i = 0; i < batch.size(); ++i) {
+      if (costs[i] < out->best_cost) {
+        out->best_cost = costs[i];
+        out->best = batch[i];
+      }
+      push_trace(out, evals, now_s() - t0, batch[i], costs[i], out->best_cost);
+      ++evals;
+    }
+  }
+  out->evals = evals;
+  out->wall_s = now_s() - t0;
+  return result;
+}
+
 }  // namespace tt

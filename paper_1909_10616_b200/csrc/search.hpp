@@ -43,6 +43,11 @@ tt_status gbfs_search(const Space& sp, const State& s0, uint64_t budget, const t
 tt_status na2c_search(const Space& sp, const State& s0, uint64_t budget, const tt_search_opts& o,
                       const BatchCost& cost, SearchOut* out, std::string* err);
 
+// Random search over the feasible set (comparator of P:64 "configurations are randomly selected to
+// be tested"): uniform without replacement, batches of `width`.
+tt_status random_search(const Space& sp, uint64_t budget, const tt_search_opts& o, const BatchCost& cost,
+                        SearchOut* out, std::string* err);
+
 State default_s0(const Space& sp);
 
 }  // namespace tt

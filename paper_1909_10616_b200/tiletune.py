@@ -98,6 +98,8 @@ EXPORTS = {
                              C.POINTER(TraceRow), u64]),
     "tt_na2c_search": (i32, [vp, i64, i64, i64, u64, C.POINTER(SearchOpts), C.POINTER(Result),
                              C.POINTER(TraceRow), u64]),
+    "tt_random_search": (i32, [vp, i64, i64, i64, u64, C.POINTER(SearchOpts), C.POINTER(Result),
+                               C.POINTER(TraceRow), u64]),
 }
 
 
@@ -371,3 +373,9 @@ def na2c_search(M: int, N: int, K: int, budget: int, opts: Optional[SearchOpts] 
                 ctx: Optional[Context] = None, **kw) -> SearchResult:
     """N-A2C (Alg. 2).  Same contract as gbfs_search."""
     return _search(lib.tt_na2c_search, "na2c_search", M, N, K, budget, opts or search_opts(), ctx, **kw)
+
+
+def random_search(M: int, N: int, K: int, budget: int, opts: Optional[SearchOpts] = None,
+                  ctx: Optional[Context] = None, **kw) -> SearchResult:
+    """Random-search comparator.  Same contract as gbfs_search."""
+    return _search(lib.tt_random_search, "random_search", M, N, K, budget, opts or search_opts(), ctx, **kw)

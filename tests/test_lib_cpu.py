@@ -238,3 +238,19 @@ def test_binding_simt_and_umma():
     with pytest.raises(tt.TileTuneError) as e:
         tt.binding(ls, space.initial_state(Spec(4096, 4096, 4096)))
     assert e.value.status == tt.E_INFEASIBLE
+
+
+@pytest.mark.parametrize("width,fam,dims", [(1, 0, (64, 64, 64)), (8, 0, (64, 64, 64)), (4, 1, (512, 512, 512))])
+def test_random_search_parity(width, fam, dims):
+    from oracle import random_search as orand
+    sp = Spec(*dims, family=fam)
+    tab = costs.table(sp, lambda s: costs.t2_cost(sp, s))
+    o = orand.random_search(sp, ogbfs.table_source(sp, tab), budget=200, seed=9, width=width)
+    m, k, n = dims
+    lres = tt.random_search(m, n, k, 200, tt.search_opts(family=fam, seed=9, width=width), table=tab)
+    assert _trace_key(lres.trace) == _oracle_key(o)
+    # whole feasible set when budget exceeds it ("evaluates the whole space")
+    small = Spec(16, 16, 16, 2, 2, 2)
+    fn = lambda s: costs.t1_cost(s, targets=((1.0, 3.0), (2.0, 2.0), (3.0, 1.0)))
+    r = tt.random_search(16, 16, 16, 1000, tt.search_opts(dm=2, dk=2, dn=2, seed=1), cost=fn)
+    assert r.evals == 125 and r.best_cost == ogbfs.brute_force(small, fn)[0]
