@@ -52,6 +52,52 @@ struct MaxThreads {
   static constexpr int value = ACC <= 16 ? 1024 : (ACC <= 64 ? 512 : 256);
 };
 
+template <int TM, int TN, bool VECA>
+__device__ __forceinline__ void load_frag(const float* as, const float* bs, int kk, int LDA, int LDB, float* a,
+                                          float* b) {
+  if constexpr (VECA) {
+#pragma unroll
+    for (int i = 0; i < TM; i += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(as + kk * LDA + i);
+      a[i] = v.x; a[i + 1] = v.y; a[i + 2] = v.z; a[i + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < TM; ++i) a[i] = as[kk * LDA + i];
+  }
+  if constexpr (TN % 4 == 0) {
+#pragma unroll
+    for (int j = 0; j < TN; j += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(bs + kk * LDB + j);
+      b[j] = v.x; b[j + 1] = v.y; b[j + 2] = v.z; b[j + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < TN; ++j) b[j] = bs[kk * LDB + j];
+  }
+}
+
+// acc[i][j] = fma(a[i], b[j], acc[i][j]) for one k step.  With PAIR the update runs as FFMA2
+// (two independent fused multiply-adds per instruction, each rounded once), so every output is
+// still exactly the fmaf chain in ascending k.
+template <int TM, int TN, bool PAIR>
+__device__ __forceinline__ void fma_frag(const float* a, const float* b, float (&acc)[TM][TN],
+                                         float2 (&acc2)[TM][PAIR ? TN / 2 : 1]) {
+  if constexpr (PAIR) {
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const float2 ai = make_float2(a[i], a[i]);
+#pragma unroll
+      for (int j = 0; j < TN / 2; ++j) acc2[i][j] = __ffma2_rn(ai, make_float2(b[2 * j], b[2 * j + 1]), acc2[i][j]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+  }
+}
+
 template <int TM, int TN>
 __global__ void __launch_bounds__(MaxThreads<TM * TN>::value)
 k1_simt(SimtArgs p) {
@@ -145,45 +191,17 @@ k1_simt(SimtArgs p) {
     __syncthreads();
     const float* as = As + buf * BK * LDA + row0;
     const float* bs = Bs + buf * BK * LDB + col0;
-#pragma unroll 2
-    for (int kk = 0; kk < BK; ++kk) {
-      float a[TM], b[TN];
-      if constexpr (kVecA) {
-#pragma unroll
-        for (int i = 0; i < TM; i += 4) {
-          const float4 v = *reinterpret_cast<const float4*>(as + kk * LDA + i);
-          a[i] = v.x; a[i + 1] = v.y; a[i + 2] = v.z; a[i + 3] = v.w;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < TM; ++i) a[i] = as[kk * LDA + i];
-      }
-      if constexpr (TN % 4 == 0) {
-#pragma unroll
-        for (int j = 0; j < TN; j += 4) {
-          const float4 v = *reinterpret_cast<const float4*>(bs + kk * LDB + j);
-          b[j] = v.x; b[j + 1] = v.y; b[j + 2] = v.z; b[j + 3] = v.w;
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < TN; ++j) b[j] = bs[kk * LDB + j];
-      }
-      if constexpr (kPair) {
-        // FFMA2: two independent fused multiply-adds per instruction, each rounded once, so
-        // every output is still the same fmaf chain in ascending k as the scalar path.
-#pragma unroll
-        for (int i = 0; i < TM; ++i) {
-          const float2 ai = make_float2(a[i], a[i]);
-#pragma unroll
-          for (int j = 0; j < TN / 2; ++j) acc2[i][j] = __ffma2_rn(ai, make_float2(b[2 * j], b[2 * j + 1]), acc2[i][j]);
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-          for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-      }
+    // fragments for step kk+1 are loaded from shared memory while step kk's FMAs issue
+    float a0[TM], b0[TN], a1[TM], b1[TN];
+    load_frag<TM, TN, kVecA>(as, bs, 0, LDA, LDB, a0, b0);
+    int kk = 0;
+    for (; kk + 2 <= BK; kk += 2) {
+      load_frag<TM, TN, kVecA>(as, bs, kk + 1, LDA, LDB, a1, b1);
+      fma_frag<TM, TN, kPair>(a0, b0, acc, acc2);
+      if (kk + 2 < BK) load_frag<TM, TN, kVecA>(as, bs, kk + 2, LDA, LDB, a0, b0);
+      fma_frag<TM, TN, kPair>(a1, b1, acc, acc2);
     }
+    if (kk < BK) fma_frag<TM, TN, kPair>(a0, b0, acc, acc2);   // odd BK: last step
     __syncthreads();
   }
   if constexpr (kPair) {
