@@ -39,6 +39,8 @@ sys.path.insert(0, ROOT)
 WORKLOADS = {
     # name: (M per rank, N, K, family, default budget)
     "bf16_4096": (4096, 4096, 4096, 3, 64),
+    # BASELINE configs[4]: 8192^3 row-partitioned; M per rank = 8192 / N GPUs (strong scaling)
+    "bf16_8192": (8192, 8192, 8192, 3, 64),
     "tf32_2048": (2048, 2048, 2048, 2, 64),
     "f32_2048": (2048, 2048, 2048, 1, 256),
     "f32_512": (512, 512, 512, 1, 484),
@@ -247,7 +249,12 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     Mr, N, K, fam, default_budget = WORKLOADS[args.workload]
-    M = Mr * world
+    strong = args.workload == "bf16_8192"
+    if strong:                       # fixed total M, rows split over the ranks
+        M = Mr
+        Mr = M // world
+    else:                            # fixed per-rank work (weak scaling)
+        M = Mr * world
     budget = args.budget if args.budget is not None else default_budget
     ctx = tt.Context(local, input_seed=1)
     sp = tt.make_space(Mr, N, K, family=fam)
@@ -375,7 +382,8 @@ def main():
         line = {
             "metric": "best-found GEMM TFLOP/s", "value": value, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": FAMILY_DTYPE[fam], "data": "synthetic",
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": FAMILY_DTYPE[fam],
+            "data": "synthetic",
             "config": {"workload": args.workload, "M_per_rank": Mr, "M_total": M, "N": N, "K": K,
                        "family": {1: "f32_simt", 2: "tf32_umma", 3: "bf16_umma"}[fam],
                        "parallelism": f"row-partitioned x{world}, candidate sharding x{world}",

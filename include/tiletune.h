@@ -142,6 +142,10 @@ typedef struct {
   double gamma, beta, lr, clip;   /* 0.9, 0.01, 0.01, 1.0 */
   int32_t epochs, minibatch, hidden;   /* 4, 64, 64 */
   int32_t rollout_cap_factor, max_t_increase;   /* 50, 16 */
+  /* T schedule ("the exploration step T can have a decay process, i.e., starting with a
+   * large value and gradually reducing to a small number"): episode e explores
+   * T_e = max(steps_T_floor, steps_T - e / steps_T_decay_every) steps; decay_every = 0: constant T. */
+  int32_t steps_T_floor, steps_T_decay_every;
 } tt_search_opts;
 
 /* How a config is bound to a launch (a5 of SURVEY §8a; for tests and reports). */

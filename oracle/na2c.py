@@ -60,11 +60,13 @@ NN_STREAM_XOR = 0xA2C0A2C0A2C0A2C0
 class Params:
     def __init__(self, steps=3, epsilon=0.8, batch=16, mem_capacity=4096, gamma=0.9, beta=0.01,
                  lr=0.01, clip=1.0, epochs=4, minibatch=64, hidden=64, rollout_cap_factor=50,
-                 max_t_increase=16):
+                 max_t_increase=16, steps_floor=1, decay_every=0):
         self.steps, self.epsilon, self.batch = steps, epsilon, batch
         self.mem_capacity, self.gamma, self.beta, self.lr, self.clip = mem_capacity, gamma, beta, lr, clip
         self.epochs, self.minibatch, self.hidden = epochs, minibatch, hidden
         self.rollout_cap_factor, self.max_t_increase = rollout_cap_factor, max_t_increase
+        # P:336 "the exploration step T can have a decay process": T_e = max(floor, T0 - e // every)
+        self.steps_floor, self.decay_every = steps_floor, decay_every
 
 
 class Agent:
@@ -149,11 +151,14 @@ def na2c(spec: space.Spec,
     memory = deque(maxlen=p.mem_capacity)
     trace = [TraceRow(0, time.perf_counter() - t0, s0, c0, best_cost)]
     cap = p.rollout_cap_factor * p.batch
+    episode = 0
 
     while evals < budget:
         if t_max is not None and time.perf_counter() - t0 >= t_max:
             break
-        T = p.steps
+        T_e = max(p.steps_floor, p.steps - episode // p.decay_every) if p.decay_every > 0 else p.steps
+        episode += 1
+        T = T_e
         coll: List[space.State] = []
         cset = set()
         exhausted = False
@@ -192,7 +197,7 @@ def na2c(spec: space.Spec,
             if coll:
                 break
             T += 1
-            if T > p.steps + p.max_t_increase:
+            if T > T_e + p.max_t_increase:
                 exhausted = True
                 break
         if exhausted:

@@ -124,7 +124,8 @@ def cmd_bench(args):
 def _run(strategy, args, seed, ctx):
     opts = tt.search_opts(family=FAMILIES[args.family], dm=args.dm, dk=args.dk, dn=args.dn, seed=seed,
                           rho=args.rho, width=args.width, steps_T=args.steps, epsilon=args.epsilon,
-                          batch=args.batch_size, gamma=args.gamma,
+                          batch=args.batch_size, gamma=args.gamma, steps_T_floor=args.steps_floor,
+                          steps_T_decay_every=args.decay_every,
                           budget_seconds=args.max_seconds or 0.0,
                           measure={"repeats": args.repeats, "warmup": args.warmup})
     if args.start_config:
@@ -221,6 +222,8 @@ def main(argv=None):
         p.add_argument("--rho", type=int, default=5)
         p.add_argument("--width", type=int, default=1)
         p.add_argument("--steps", type=int, default=3)
+        p.add_argument("--steps-floor", type=int, default=1, help="T decay floor (P:336)")
+        p.add_argument("--decay-every", type=int, default=0, help="decrease T by 1 every this many episodes")
         p.add_argument("--epsilon", type=float, default=0.8)
         p.add_argument("--batch-size", type=int, default=16)
         p.add_argument("--gamma", type=float, default=0.9)

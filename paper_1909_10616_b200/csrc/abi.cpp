@@ -175,6 +175,8 @@ void tt_search_opts_default(tt_search_opts* o) {
   o->hidden = 64;
   o->rollout_cap_factor = 50;
   o->max_t_increase = 16;
+  o->steps_T_floor = 1;
+  o->steps_T_decay_every = 0;
 }
 
 tt_status tt_count_configs(const tt_space* sp, uint64_t* raw, uint64_t* feasible) {

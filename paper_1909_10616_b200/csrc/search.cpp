@@ -269,6 +269,8 @@ tt_status na2c_search(const Space& sp, const State& s0, uint64_t budget, const t
   const int minibatch = o.minibatch > 0 ? o.minibatch : 64;
   const int capf = o.rollout_cap_factor > 0 ? o.rollout_cap_factor : 50;
   const int maxinc = o.max_t_increase >= 0 ? o.max_t_increase : 16;
+  const int Tfloor = o.steps_T_floor > 0 ? o.steps_T_floor : 1;
+  int64_t episode = 0;
 
   SplitMix64 rng(o.seed);
   SplitMix64 rng_nn(o.seed ^ 0xA2C0A2C0A2C0A2C0ull);
@@ -304,7 +306,10 @@ tt_status na2c_search(const Space& sp, const State& s0, uint64_t budget, const t
 
   while (evals < budget) {
     if (o.budget_seconds > 0 && now_s() - t0 >= o.budget_seconds) break;
-    int T = T0;
+    // P:336 decay schedule: T_e = max(floor, T0 - e / decay_every) (constant when decay_every = 0)
+    const int Te = o.steps_T_decay_every > 0 ? (int)std::max<int64_t>(Tfloor, T0 - episode / o.steps_T_decay_every) : T0;
+    ++episode;
+    int T = Te;
     std::vector<State> coll;
     std::unordered_set<uint64_t> cset;
     bool exhausted = false;
@@ -349,7 +354,7 @@ tt_status na2c_search(const Space& sp, const State& s0, uint64_t budget, const t
         }
       }
       if (!coll.empty()) break;
-      if (++T > T0 + maxinc) { exhausted = true; break; }                 // P:336 increase T
+      if (++T > Te + maxinc) { exhausted = true; break; }                 // P:336 increase T
     }
     if (exhausted) break;
     if (coll.size() > budget - evals) coll.resize(budget - evals);

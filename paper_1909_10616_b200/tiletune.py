@@ -62,7 +62,7 @@ class SearchOpts(C.Structure):
                 ("measure", MeasureOpts), ("rho", i32), ("width", i32), ("steps_T", i32), ("epsilon", dbl),
                 ("batch", i32), ("mem_capacity", i32), ("gamma", dbl), ("beta", dbl), ("lr", dbl), ("clip", dbl),
                 ("epochs", i32), ("minibatch", i32), ("hidden", i32), ("rollout_cap_factor", i32),
-                ("max_t_increase", i32)]
+                ("max_t_increase", i32), ("steps_T_floor", i32), ("steps_T_decay_every", i32)]
 
 
 class LaunchInfo(C.Structure):

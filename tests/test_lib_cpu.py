@@ -254,3 +254,17 @@ def test_random_search_parity(width, fam, dims):
     fn = lambda s: costs.t1_cost(s, targets=((1.0, 3.0), (2.0, 2.0), (3.0, 1.0)))
     r = tt.random_search(16, 16, 16, 1000, tt.search_opts(dm=2, dk=2, dn=2, seed=1), cost=fn)
     assert r.evals == 125 and r.best_cost == ogbfs.brute_force(small, fn)[0]
+
+
+def test_na2c_T_decay_schedule_parity():
+    # P:336 decay process: T_e = max(floor, T0 - e // every); eps = 0 keeps the traversal exact
+    sp = Spec(64, 64, 64)
+    tab = costs.table(sp, lambda s: costs.t2_cost(sp, s))
+    p = ona2c.Params(epsilon=0.0, steps=8, steps_floor=2, decay_every=3, batch=6)
+    o = ona2c.na2c(sp, ogbfs.table_source(sp, tab), budget=250, params=p, seed=2)
+    lres = tt.na2c_search(64, 64, 64, 250, tt.search_opts(seed=2, epsilon=0.0, steps_T=8, steps_T_floor=2,
+                                                          steps_T_decay_every=3, batch=6), table=tab)
+    assert _trace_key(lres.trace) == _oracle_key(o)
+    # the schedule changes the traversal relative to a constant T = 8
+    const = tt.na2c_search(64, 64, 64, 250, tt.search_opts(seed=2, epsilon=0.0, steps_T=8, batch=6), table=tab)
+    assert _trace_key(const.trace) != _trace_key(lres.trace)
