@@ -221,6 +221,8 @@ def main():
     ap.add_argument("--workload", default="bf16_4096", choices=sorted(WORKLOADS))
     ap.add_argument("--budget", type=int, default=None, help="G-BFS evaluation budget (distinct configs)")
     ap.add_argument("--width", type=int, default=8)
+    ap.add_argument("--layout", choices=["nn", "tn"], default="nn",
+                    help="tn: A stored as W[K][M] (the paper's perceptron Y = W^T X, P:372)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--ref-rows", type=int, default=16)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -257,7 +259,8 @@ def main():
         M = Mr * world
     budget = args.budget if args.budget is not None else default_budget
     ctx = tt.Context(local, input_seed=1)
-    sp = tt.make_space(Mr, N, K, family=fam)
+    layout = tt.LAYOUT_TN if args.layout == "tn" else tt.LAYOUT_NN
+    sp = tt.make_space(Mr, N, K, family=fam, layout=layout)
     raw, feasible = tt.count_configs(sp, feasible=True)
 
     # ---------------- 1. tuning pass (G-BFS, candidates sharded over ranks) ----------------
@@ -270,7 +273,7 @@ def main():
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        res = tt.gbfs_search(Mr, N, K, budget, tt.search_opts(family=fam, seed=args.seed, width=args.width), batch=ev)
+        res = tt.gbfs_search(Mr, N, K, budget, tt.search_opts(family=fam, seed=args.seed, width=args.width, layout=layout), batch=ev)
         tune_wall = tdist.max_over_ranks(time.perf_counter() - t0, dev)
         best = res.best
         tune = {"algorithm": "G-BFS (Alg. 1, width %d, rho 5)" % args.width, "budget": budget, "evals": res.evals,
@@ -283,10 +286,13 @@ def main():
     # ---------------- 2. timed steps of the best-found GEMM on this rank's row shard ----------
     bf16 = fam == 3
     r0, r1 = tdist.row_shard(M, world, rank)
-    A = torch.empty(Mr, K, device=dev, dtype=torch.bfloat16 if bf16 else torch.float32)
+    tn = layout == tt.LAYOUT_TN
+    # NN: A rows are global rows r0.. of the full A.  TN: each rank's W shard [K][Mr] is its own
+    # recipe block (index offset rank * K * Mr): the row blocks of Y = W^T X are independent.
+    A = torch.empty((K, Mr) if tn else (Mr, K), device=dev, dtype=torch.bfloat16 if bf16 else torch.float32)
     B = torch.empty(K, N, device=dev, dtype=A.dtype)
     C = torch.empty(Mr, N, device=dev, dtype=torch.float32)
-    tt.fill_uniform(A, seed=1, idx0=r0 * K)        # global row indices: shards == rows of the full A
+    tt.fill_uniform(A, seed=1, idx0=r0 * K)        # NN: global row indices; TN: rank block offset
     tt.fill_uniform(B, seed=2)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
@@ -294,7 +300,7 @@ def main():
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     for _ in range(args.warmup):
         flush.fill_(1)
-        tt.gemm(A, B, C, fam, best)
+        tt.gemm(A, B, C, fam, best, layout=layout)
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
@@ -304,7 +310,7 @@ def main():
     for i in range(args.steps):
         flush.fill_(i & 0xFF)                           # L2 flush between steps (outside the events)
         starts[i].record(stream)
-        tt.gemm(A, B, C, fam, best)
+        tt.gemm(A, B, C, fam, best, layout=layout)
         ends[i].record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -324,7 +330,11 @@ def main():
     ii = np.array([0, Mr // 3, Mr - 1])
     jj = np.array([N - 1, N // 2, 0])
     Ah = synth.uniform_f32(1, 3, K, row0=0)
-    Arows = np.stack([synth.uniform_f32(1, 1, K, row0=r0 + int(i))[0] for i in ii])
+    if tn:
+        Wsh = synth.uniform_f32(1, K, Mr, row0=r0 * K // Mr)      # the rank's W block
+        Arows = np.stack([Wsh[:, int(i)] for i in ii])
+    else:
+        Arows = np.stack([synth.uniform_f32(1, 1, K, row0=r0 + int(i))[0] for i in ii])
     Bh = synth.uniform_f32(2, K, N)
     if bf16:
         Arows = synth.bf16_bits_to_f32(synth.to_bf16_bits(Arows))
@@ -338,13 +348,13 @@ def main():
     Ah_t = A.cpu().pin_memory()
     Bh_t = B.cpu().pin_memory()
     Ch_t = torch.empty(Mr, N, dtype=torch.float32).pin_memory()
-    ctx.gemm_host(Ah_t, Bh_t, Ch_t, fam, best)       # warm (allocates staging)
+    ctx.gemm_host(Ah_t, Bh_t, Ch_t, fam, best, layout=layout)       # warm (allocates staging)
     e2e_steps = min(args.steps, 5)
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        ctx.gemm_host(Ah_t, Bh_t, Ch_t, fam, best)
+        ctx.gemm_host(Ah_t, Bh_t, Ch_t, fam, best, layout=layout)
     e2e_s = tdist.max_over_ranks((time.perf_counter() - t0) / e2e_steps, dev)
     e2e_val = world * flops_rank / e2e_s / 1e12
     h2d = Ah_t.numel() * Ah_t.element_size() + Bh_t.numel() * Bh_t.element_size()
@@ -385,6 +395,7 @@ def main():
             "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": FAMILY_DTYPE[fam],
             "data": "synthetic",
             "config": {"workload": args.workload, "M_per_rank": Mr, "M_total": M, "N": N, "K": K,
+                       "layout": args.layout,
                        "family": {1: "f32_simt", 2: "tf32_umma", 3: "bf16_umma"}[fam],
                        "parallelism": f"row-partitioned x{world}, candidate sharding x{world}",
                        "l2": "flushed (256 MiB memset) before every timed launch",

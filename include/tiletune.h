@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define TT_VERSION 1
+#define TT_VERSION 2
 #define TT_MAXD 4  /* maximum loop depth per axis carried in tt_config */
 
 typedef enum {
@@ -51,11 +51,17 @@ typedef enum {
   TT_FAM_BF16_UMMA = 3     /* K3: tcgen05.mma kind::f16 with bf16 A/B, fp32 accumulate */
 } tt_family;
 
+/* Storage of A.  NN: A row-major [M][K] (the plain definition, reading Z14).  TN: the paper's
+ * perceptron workload Y = W^T X with W in R^(k x m): the caller passes W row-major
+ * [K][M] and the product uses A = W^T.  B is always row-major [K][N]. */
+typedef enum { TT_LAYOUT_NN = 0, TT_LAYOUT_TN = 1 } tt_layout;
+
 /* Problem instance: the paper's cost(s; m,k,n,d_m,d_k,d_n), plus the J_hw family. */
 typedef struct {
   int64_t M, N, K;         /* C[M x N] = A[M x K] B[K x N]; all >= 1 */
   int32_t dm, dk, dn;      /* loop depths d_m, d_k, d_n, 1..TT_MAXD; paper uses 4,2,4 */
   int32_t family;          /* tt_family */
+  int32_t layout;          /* tt_layout of A (does not change the space or J_hw, only the kernel) */
 } tt_space;
 
 /* A state s = [s_m, s_k, s_n] (Eq. 5).  Factor vectors outer -> inner (reading Z1):
@@ -146,6 +152,7 @@ typedef struct {
    * large value and gradually reducing to a small number"): episode e explores
    * T_e = max(steps_T_floor, steps_T - e / steps_T_decay_every) steps; decay_every = 0: constant T. */
   int32_t steps_T_floor, steps_T_decay_every;
+  int32_t layout;          /* tt_layout of A for the DEVICE cost source (default NN) */
 } tt_search_opts;
 
 /* How a config is bound to a launch (a5 of SURVEY §8a; for tests and reports). */
@@ -224,9 +231,15 @@ tt_status tt_fill_uniform(void* dst, int32_t dtype, uint64_t seed, uint64_t idx0
 tt_status tt_gemm(int64_t M, int64_t N, int64_t K, int32_t family, const void* A, const void* B,
                   float* C, const tt_config* cfg, void* stream);
 
-/* Same product through host buffers: copies A, B host->device, runs tt_gemm, copies C back,
- * all on the ctx stream, and synchronises.  The ctx owns the device staging buffers. */
-tt_status tt_gemm_host(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, int32_t family,
+/* tt_gemm with an explicit A storage (tt_layout): for TT_LAYOUT_TN, A points to W row-major
+ * [K][M] and C = W^T B.  Alignment as tt_gemm (UMMA families also need M a multiple of 8). */
+tt_status tt_gemm_ex(int64_t M, int64_t N, int64_t K, int32_t family, int32_t layout, const void* A,
+                     const void* B, float* C, const tt_config* cfg, void* stream);
+
+/* Same product through host buffers: copies A (stored per `layout`), B host->device, runs the
+ * GEMM, copies C back, all on the ctx stream, and synchronises.  The ctx owns the device staging
+ * buffers.  Host buffers should be pinned for asynchronous copies. */
+tt_status tt_gemm_host(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, int32_t family, int32_t layout,
                        const void* A_host, const void* B_host, float* C_host, const tt_config* cfg);
 
 /* ---------------------------------------------------------------- measurement (B2) */

@@ -91,8 +91,11 @@ def synthetic_cost(args):
     return f
 
 
+LAYOUTS = {"nn": tt.LAYOUT_NN, "tn": tt.LAYOUT_TN}
+
+
 def _space(args):
-    return tt.make_space(args.m, args.n, args.k, args.dm, args.dk, args.dn, FAMILIES[args.family])
+    return tt.make_space(args.m, args.n, args.k, args.dm, args.dk, args.dn, FAMILIES[args.family], LAYOUTS[args.layout])
 
 
 def cmd_count(args):
@@ -125,7 +128,7 @@ def _run(strategy, args, seed, ctx):
     opts = tt.search_opts(family=FAMILIES[args.family], dm=args.dm, dk=args.dk, dn=args.dn, seed=seed,
                           rho=args.rho, width=args.width, steps_T=args.steps, epsilon=args.epsilon,
                           batch=args.batch_size, gamma=args.gamma, steps_T_floor=args.steps_floor,
-                          steps_T_decay_every=args.decay_every,
+                          steps_T_decay_every=args.decay_every, layout=LAYOUTS[args.layout],
                           budget_seconds=args.max_seconds or 0.0,
                           measure={"repeats": args.repeats, "warmup": args.warmup})
     if args.start_config:
@@ -193,6 +196,8 @@ def main(argv=None):
         p.add_argument("--dn", type=int, default=4)
         p.add_argument("--family", choices=sorted(FAMILIES), default="none")
         p.add_argument("--device", type=int, default=0)
+        p.add_argument("--layout", choices=["nn", "tn"], default="nn",
+                       help="tn: A given as W[k][m], the paper's Y = W^T X (P:372)")
 
     p = sub.add_parser("count")
     common(p)

@@ -39,6 +39,7 @@ tt_space make_space(int64_t M, int64_t N, int64_t K, const tt_search_opts* o) {
   s.dk = o->dk > 0 ? o->dk : 2;
   s.dn = o->dn > 0 ? o->dn : 4;
   s.family = o->family;
+  s.layout = o->layout;
   return s;
 }
 
@@ -177,6 +178,7 @@ void tt_search_opts_default(tt_search_opts* o) {
   o->max_t_increase = 16;
   o->steps_T_floor = 1;
   o->steps_T_decay_every = 0;
+  o->layout = TT_LAYOUT_NN;
 }
 
 tt_status tt_count_configs(const tt_space* sp, uint64_t* raw, uint64_t* feasible) {
@@ -305,9 +307,9 @@ tt_status tt_fill_uniform(void* dst, int32_t dtype, uint64_t seed, uint64_t idx0
   return r == TT_OK ? TT_OK : fail(r, err);
 }
 
-tt_status tt_gemm(int64_t M, int64_t N, int64_t K, int32_t family, const void* A, const void* B, float* C,
-                  const tt_config* cfg, void* stream) {
-  tt_space ts{M, N, K, 4, 2, 4, family};
+tt_status tt_gemm_ex(int64_t M, int64_t N, int64_t K, int32_t family, int32_t layout, const void* A, const void* B,
+                     float* C, const tt_config* cfg, void* stream) {
+  tt_space ts{M, N, K, 4, 2, 4, family, layout};
   CHECK_SPACE(&ts);
   if (!A || !B || !C || !cfg) return fail(TT_E_INVAL, "null argument");
   if (family == TT_FAM_NONE) return fail(TT_E_UNSUPPORTED, "family NONE has no kernel");
@@ -318,6 +320,11 @@ tt_status tt_gemm(int64_t M, int64_t N, int64_t K, int32_t family, const void* A
   std::string err;
   tt_status r = launch_gemm(s, st, A, B, C, static_cast<cudaStream_t>(stream), &err);
   return r == TT_OK ? TT_OK : fail(r, err);
+}
+
+tt_status tt_gemm(int64_t M, int64_t N, int64_t K, int32_t family, const void* A, const void* B, float* C,
+                  const tt_config* cfg, void* stream) {
+  return tt_gemm_ex(M, N, K, family, TT_LAYOUT_NN, A, B, C, cfg, stream);
 }
 
 tt_status tt_ctx_create(int32_t device, uint64_t input_seed, tt_ctx** out) {
@@ -349,7 +356,7 @@ tt_status tt_ctx_stream(tt_ctx* ctx, void** stream) {
 tt_status tt_ctx_operands(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, int32_t family, const void** A,
                           const void** B, float** C) {
   if (!ctx) return fail(TT_E_INVAL, "null ctx");
-  tt_space ts{M, N, K, 4, 2, 4, family};
+  tt_space ts{M, N, K, 4, 2, 4, family, TT_LAYOUT_NN};
   CHECK_SPACE(&ts);
   Space s(ts, false);
   Operands* o = nullptr;
@@ -362,10 +369,10 @@ tt_status tt_ctx_operands(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, int32_t 
   return TT_OK;
 }
 
-tt_status tt_gemm_host(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, int32_t family, const void* A_host,
-                       const void* B_host, float* C_host, const tt_config* cfg) {
+tt_status tt_gemm_host(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, int32_t family, int32_t layout,
+                       const void* A_host, const void* B_host, float* C_host, const tt_config* cfg) {
   if (!ctx || !A_host || !B_host || !C_host || !cfg) return fail(TT_E_INVAL, "null argument");
-  tt_space ts{M, N, K, 4, 2, 4, family};
+  tt_space ts{M, N, K, 4, 2, 4, family, layout};
   CHECK_SPACE(&ts);
   Space s(ts, false);
   State st = from_cfg(*cfg);

@@ -32,6 +32,8 @@ struct SimtArgs {
   int m1, m2, n1, n2, bk, k0;
   int bk_sh;  // log2(BK) if BK is a power of two, else -1
   int bq_sh;  // log2(BN / 4) if a power of two, else -1
+  int a_tn;   // A stored as W = A^T row-major [K][M] (the paper's Y = W^T X)
+  int a_vec16;  // TN: 16-byte cp.async of W rows legal
   int b_vec;  // B rows 16-byte aligned (16-byte cp.async legal)
 };
 
@@ -119,7 +121,8 @@ k1_simt(SimtArgs p) {
   const int col0 = gn * (p.n2 * TN) + ln * TN;
 
   const int64_t K = p.K, N = p.N;
-  const float* Ab = p.A + (int64_t)blockIdx.y * BM * K;
+  const float* Ab = p.a_tn ? p.A + (int64_t)blockIdx.y * BM : p.A + (int64_t)blockIdx.y * BM * K;
+  const int64_t M = p.M;
   const float* Bb = p.B + (int64_t)blockIdx.x * BN;
 
   auto load = [&](int kt, int buf) {
@@ -127,7 +130,20 @@ k1_simt(SimtArgs p) {
     float* bs = Bs + buf * BK * LDB;
     const int64_t kb = (int64_t)kt * BK;
     const int na = BM * BK;
-    if (p.bk_sh >= 0) {                    // power-of-two BK: shifts instead of divisions
+    if (p.a_tn) {                          // W rows are already k-major: As[k][m] needs no transpose
+      if (p.a_vec16) {
+        const int q = BM >> 2;
+        for (int e = t; e < BK * q; e += T) {
+          const int r = e / q, c = (e - (e / q) * q) << 2;
+          cp_async16(as + r * LDA + c, Ab + (kb + r) * M + c);
+        }
+      } else {
+        for (int e = t; e < BK * BM; e += T) {
+          const int r = e / BM, c = e - (e / BM) * BM;
+          cp_async4(as + r * LDA + c, Ab + (kb + r) * M + c);
+        }
+      }
+    } else if (p.bk_sh >= 0) {             // power-of-two BK: shifts instead of divisions
       for (int e = t; e < na; e += T) {
         const int r = e >> p.bk_sh, c = e & (BK - 1);
         cp_async4(as + c * LDA + r, Ab + (int64_t)r * K + kb + c);
@@ -324,6 +340,9 @@ tt_status simt_launch(const Space& sp, const State& s, const float* A, const flo
   a.bk_sh = lg(a.bk);
   a.bq_sh = (li.tile_n % 4 == 0) ? lg(li.tile_n / 4) : -1;
   a.b_vec = (li.tile_n % 4 == 0 && a.N % 4 == 0 && ((uintptr_t)B % 16) == 0) ? 1 : 0;
+  a.a_tn = sp.layout == TT_LAYOUT_TN ? 1 : 0;
+  a.a_vec16 = (li.tile_m % 4 == 0 && a.M % 4 == 0 && ((uintptr_t)A % 16) == 0 &&
+               ((2 * (int64_t)a.bk * (li.tile_n + 4)) % 4) == 0) ? 1 : 0;
   dim3 grid((unsigned)li.grid_x, (unsigned)li.grid_y, 1);
   fn<<<grid, li.block_x, li.smem_bytes, stream>>>(a);
   if (!cuda_ok(cudaGetLastError(), err, "k1_simt launch")) return TT_E_CUDA;

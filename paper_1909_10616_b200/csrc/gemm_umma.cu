@@ -39,6 +39,8 @@ struct UmmaArgs {
   int swz_a, swz_b;                 // swizzle bytes: 32 | 64 | 128
   int a_layout, b_layout;           // descriptor layout codes (SW128 2, SW64 4, SW32 6, SW128_BASE32B 1)
   int sbo_b;                        // B stride between K core-matrix groups (bytes)
+  int a_mn;                         // A is MN-major: W = A^T row-major [K][M] (P:372 Y = W^T X)
+  int a_cw;                         // MN-major A: M elements per TMA box (128 B)
   int a_chunk_bytes;                // bytes of one A K-chunk (rows x swz_a)
   int b_cw;                         // B columns per TMA box (swz_b / elem)
   int nb;                           // B columns per CTA per atom = n3 / cta_group
@@ -194,6 +196,9 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+template <int KIND>
+__device__ __forceinline__ constexpr uint32_t kind_sbo_mn() { return KIND == 1 ? 4u * 128u : 8u * 128u; }
+
 struct MmaCtx {
   uint32_t sbase, full0, empty0, tfull0, tempty0, tmem_base;
   int cluster_id, num_clusters, num_tiles;
@@ -205,9 +210,13 @@ __device__ __forceinline__ void mma_role(const UmmaArgs& p, const MmaCtx& c) {
   constexpr int UK = KIND == 0 ? 16 : 8;
   // descriptor words: high halves are invariant; low halves = (start >> 4) | (LBO >> 4) << 16
   const uint32_t lbo_b = (uint32_t)(p.bk * p.swz_b);
-  const uint64_t a_hi = smem_desc(0, 16u, 8u * (uint32_t)p.swz_a, p.a_layout) & 0xFFFFFFFF00000000ull;
+  // K-major A: 128-row atoms of swz_a-byte rows; MN-major A (TN layout): BK x 128 B boxes of a_cw
+  // rows each, atom mi = 128 / a_cw boxes, LBO = box stride, SBO = 8 (4 for tf32) K-rows x 128 B
+  const uint32_t a_box = (uint32_t)(p.bk * 128);
+  const uint64_t a_hi = (p.a_mn ? smem_desc(0, a_box, kind_sbo_mn<KIND>(), p.a_layout)
+                                : smem_desc(0, 16u, 8u * (uint32_t)p.swz_a, p.a_layout)) & 0xFFFFFFFF00000000ull;
   const uint64_t b_hi = smem_desc(0, lbo_b, (uint32_t)p.sbo_b, p.b_layout) & 0xFFFFFFFF00000000ull;
-  const uint32_t a_lbo = 1u << 16;
+  const uint32_t a_lbo = p.a_mn ? (((a_box >> 4) & 0x3FFFu) << 16) : (1u << 16);
   const uint32_t b_lbo = ((lbo_b >> 4) & 0x3FFFu) << 16;
   uint32_t a_off[KS][M2], b_off[KS][N2], d_off[M2][N2];
 #pragma unroll
@@ -215,7 +224,9 @@ __device__ __forceinline__ void mma_role(const UmmaArgs& p, const MmaCtx& c) {
     const uint32_t kbytes = (uint32_t)(ks * UK * ELEM);
 #pragma unroll
     for (int mi = 0; mi < M2; ++mi)
-      a_off[ks][mi] = (((kbytes / p.swz_a) * p.a_chunk_bytes + kbytes % p.swz_a + mi * 128 * p.swz_a) >> 4) | a_lbo;
+      a_off[ks][mi] = p.a_mn
+          ? (((uint32_t)(mi * (128 / p.a_cw)) * a_box + (uint32_t)(ks * UK * 128)) >> 4) | a_lbo
+          : (((kbytes / p.swz_a) * p.a_chunk_bytes + kbytes % p.swz_a + mi * 128 * p.swz_a) >> 4) | a_lbo;
 #pragma unroll
     for (int ni = 0; ni < N2; ++ni)
       b_off[ks][ni] = (((uint32_t)(ni * (p.nb / p.b_cw)) * lbo_b + (uint32_t)(ks * UK * p.swz_b)) >> 4) | b_lbo;
@@ -336,8 +347,13 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
           if (leader) mbar_arrive_expect_tx(fb, p.tx_bytes * CG);
           const uint32_t sa = sbase + (uint32_t)stage * p.stage_bytes;
           const uint32_t sb = sa + p.a_stage_bytes;
-          for (int kc = 0; kc < kchunks; ++kc)
-            tma_load_2d<CG>(&tmA, fb, sa + kc * p.a_chunk_bytes, kb * p.bk + kc * a_kstep, row);
+          if (p.a_mn) {                                    // W rows: boxes of a_cw M-elements x BK
+            for (int c = 0; c < rows_cta / p.a_cw; ++c)
+              tma_load_2d<CG>(&tmA, fb, sa + (uint32_t)c * (uint32_t)(p.bk * 128), row + c * p.a_cw, kb * p.bk);
+          } else {
+            for (int kc = 0; kc < kchunks; ++kc)
+              tma_load_2d<CG>(&tmA, fb, sa + kc * p.a_chunk_bytes, kb * p.bk + kc * a_kstep, row);
+          }
           for (int ni = 0; ni < p.n2; ++ni)
             for (int c = 0; c < bboxes; ++c)
               tma_load_2d<CG>(&tmB, fb, sb + (uint32_t)(ni * bboxes + c) * bbox_bytes, colt + ni * p.n3 + c * p.b_cw,
@@ -541,7 +557,10 @@ void plan_of(const Space& sp, const State& s, Plan* pl) {
   // instruction descriptor: F32 accum, A/B format, A K-major, B MN-major, N>>3, M>>4
   const uint32_t fmt = kind == 0 ? 1u : 2u;
   const uint32_t M_inst = 128u * (uint32_t)m1;
-  a.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (0u << 15) | (1u << 16) | (((uint32_t)a.n3 >> 3) << 17) |
+  a.a_mn = sp.layout == TT_LAYOUT_TN ? 1 : 0;
+  a.a_cw = 128 / elem;
+  if (a.a_mn) a.a_layout = kind == 1 ? 1 : 2;          // MN-major A: SW128 (tf32: 32B atoms)
+  a.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)a.a_mn << 15) | (1u << 16) | (((uint32_t)a.n3 >> 3) << 17) |
             ((M_inst >> 4) << 24);
   pl->cg = m1;
   pl->kind = kind;
@@ -612,12 +631,16 @@ tt_status umma_launch(const Space& sp, const State& s, const void* A, const void
     return TT_E_INVAL;
   }
   const int elem = pl.kind == 0 ? 2 : 4;
-  if ((pl.a.K * elem) % 16 || (pl.a.N * elem) % 16) {
+  if ((pl.a.K * elem) % 16 || (pl.a.N * elem) % 16 || (pl.a.a_mn && (pl.a.M * elem) % 16)) {
     *err = "UMMA family needs row pitches that are multiples of 16 bytes";
     return TT_E_UNSUPPORTED;
   }
   CUtensorMap ma, mb, mc;
-  if (!make_map(&ma, pl.kind, A, (uint64_t)pl.a.K, (uint64_t)pl.a.M, (uint32_t)(pl.a.swz_a / elem),
+  if (pl.a.a_mn) {
+    if (!make_map(&ma, pl.kind, A, (uint64_t)pl.a.M, (uint64_t)pl.a.K, (uint32_t)pl.a.a_cw, (uint32_t)pl.a.bk,
+                  pl.kind == 1 ? -128 : 128, err))
+      return TT_E_CUDA;
+  } else if (!make_map(&ma, pl.kind, A, (uint64_t)pl.a.K, (uint64_t)pl.a.M, (uint32_t)(pl.a.swz_a / elem),
                 (uint32_t)(pl.a.m2 * 128), pl.a.swz_a, err))
     return TT_E_CUDA;
   if (!make_map(&mb, pl.kind, B, (uint64_t)pl.a.N, (uint64_t)pl.a.K, (uint32_t)pl.a.b_cw, (uint32_t)pl.a.bk,

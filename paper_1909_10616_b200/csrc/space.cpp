@@ -84,6 +84,7 @@ Space::Space(const tt_space& sp, bool build_lists) {
   d[1] = sp.dk;
   d[2] = sp.dn;
   family = sp.family;
+  layout = sp.layout;
   for (int a = 0; a < 3; ++a)
     for (int i = 0; i < d[a]; ++i)
       for (int j = 0; j < d[a]; ++j)
@@ -100,8 +101,8 @@ Space::Space(const tt_space& sp, bool build_lists) {
 
 std::shared_ptr<const Space> Space::get(const tt_space& sp) {
   static std::mutex mu;
-  static std::map<std::tuple<int64_t, int64_t, int64_t, int, int, int, int>, std::shared_ptr<const Space>> cache;
-  auto key = std::make_tuple(sp.M, sp.N, sp.K, sp.dm, sp.dk, sp.dn, sp.family);
+  static std::map<std::tuple<int64_t, int64_t, int64_t, int, int, int, int, int>, std::shared_ptr<const Space>> cache;
+  auto key = std::make_tuple(sp.M, sp.N, sp.K, sp.dm, sp.dk, sp.dn, sp.family, sp.layout);
   std::lock_guard<std::mutex> lk(mu);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
@@ -258,6 +259,7 @@ bool valid_space(const tt_space* sp, std::string* why) {
     return false;
   }
   if (sp->family < TT_FAM_NONE || sp->family > TT_FAM_BF16_UMMA) { *why = "unknown family"; return false; }
+  if (sp->layout != TT_LAYOUT_NN && sp->layout != TT_LAYOUT_TN) { *why = "unknown layout"; return false; }
   return true;
 }
 

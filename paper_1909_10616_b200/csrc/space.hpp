@@ -31,6 +31,7 @@ class Space {
   int64_t dim[3];
   int d[3];
   int family;
+  int layout;  // tt_layout of A (kernel selection only)
   std::vector<Vec> lists[3];
   std::vector<Action> actions;  // fixed order: axis, i asc, j asc, j != i
 

@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(HERE, "libtiletune.so")
 
 OK, E_INVAL, E_ILLEGITIMATE, E_INFEASIBLE, E_OVERFLOW, E_CAPACITY, E_CUDA, E_EVALUATOR, E_UNSUPPORTED = range(9)
 FAM_NONE, FAM_F32_SIMT, FAM_TF32_UMMA, FAM_BF16_UMMA = 0, 1, 2, 3
+LAYOUT_NN, LAYOUT_TN = 0, 1
 COST_DEVICE, COST_CALLBACK, COST_TABLE, COST_BATCH = 0, 1, 2, 3
 MAXD = 4
 
@@ -24,7 +25,8 @@ i32, i64, u32, u64, dbl, vp = C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_
 
 
 class Space(C.Structure):
-    _fields_ = [("M", i64), ("N", i64), ("K", i64), ("dm", i32), ("dk", i32), ("dn", i32), ("family", i32)]
+    _fields_ = [("M", i64), ("N", i64), ("K", i64), ("dm", i32), ("dk", i32), ("dn", i32), ("family", i32),
+                ("layout", i32)]
 
 
 class Config(C.Structure):
@@ -62,7 +64,7 @@ class SearchOpts(C.Structure):
                 ("measure", MeasureOpts), ("rho", i32), ("width", i32), ("steps_T", i32), ("epsilon", dbl),
                 ("batch", i32), ("mem_capacity", i32), ("gamma", dbl), ("beta", dbl), ("lr", dbl), ("clip", dbl),
                 ("epochs", i32), ("minibatch", i32), ("hidden", i32), ("rollout_cap_factor", i32),
-                ("max_t_increase", i32), ("steps_T_floor", i32), ("steps_T_decay_every", i32)]
+                ("max_t_increase", i32), ("steps_T_floor", i32), ("steps_T_decay_every", i32), ("layout", i32)]
 
 
 class LaunchInfo(C.Structure):
@@ -88,7 +90,8 @@ EXPORTS = {
     "tt_binding": (i32, [C.POINTER(Space), C.POINTER(Config), C.POINTER(LaunchInfo)]),
     "tt_fill_uniform": (i32, [vp, i32, u64, u64, u64, vp]),
     "tt_gemm": (i32, [i64, i64, i64, i32, vp, vp, vp, C.POINTER(Config), vp]),
-    "tt_gemm_host": (i32, [vp, i64, i64, i64, i32, vp, vp, vp, C.POINTER(Config)]),
+    "tt_gemm_ex": (i32, [i64, i64, i64, i32, i32, vp, vp, vp, C.POINTER(Config), vp]),
+    "tt_gemm_host": (i32, [vp, i64, i64, i64, i32, i32, vp, vp, vp, C.POINTER(Config)]),
     "tt_ctx_create": (i32, [i32, u64, C.POINTER(vp)]),
     "tt_ctx_destroy": (i32, [vp]),
     "tt_ctx_stream": (i32, [vp, C.POINTER(vp)]),
@@ -134,8 +137,9 @@ def _check(st: int, where: str):
 State = Tuple[Tuple[int, ...], Tuple[int, ...], Tuple[int, ...]]
 
 
-def make_space(M: int, N: int, K: int, dm: int = 4, dk: int = 2, dn: int = 4, family: int = FAM_NONE) -> Space:
-    return Space(M, N, K, dm, dk, dn, family)
+def make_space(M: int, N: int, K: int, dm: int = 4, dk: int = 2, dn: int = 4, family: int = FAM_NONE,
+               layout: int = LAYOUT_NN) -> Space:
+    return Space(M, N, K, dm, dk, dn, family, layout)
 
 
 def to_config(s: State) -> Config:
@@ -235,13 +239,17 @@ def fill_uniform(tensor, seed: int, idx0: int = 0, stream=None):
     _check(lib.tt_fill_uniform(tensor.data_ptr(), dt, seed, idx0, tensor.numel(), _stream(stream)), "fill_uniform")
 
 
-def gemm(A, B, C_out, family: int, s: State, stream=None):
-    """C_out[M,N] (fp32) = A[M,K] . B[K,N] with config s on the device (tt_gemm)."""
-    M, K = A.shape
+def gemm(A, B, C_out, family: int, s: State, stream=None, layout: int = LAYOUT_NN):
+    """C_out[M,N] (fp32) = A[M,K] . B[K,N] with config s on the device (tt_gemm_ex).  With
+    layout=LAYOUT_TN, A is passed as W = A^T of shape [K, M] (P:372 Y = W^T X)."""
+    if layout == LAYOUT_TN:
+        K, M = A.shape
+    else:
+        M, K = A.shape
     K2, N = B.shape
     assert K == K2 and tuple(C_out.shape) == (M, N)
-    _check(lib.tt_gemm(M, N, K, family, A.data_ptr(), B.data_ptr(), C_out.data_ptr(), C.byref(to_config(s)),
-                       _stream(stream)), "gemm")
+    _check(lib.tt_gemm_ex(M, N, K, family, layout, A.data_ptr(), B.data_ptr(), C_out.data_ptr(),
+                          C.byref(to_config(s)), _stream(stream)), "gemm")
 
 
 def measure_opts(**kw) -> MeasureOpts:
@@ -287,11 +295,11 @@ class Context:
                               C.byref(out)), "measure")
         return out
 
-    def gemm_host(self, A_host, B_host, C_host, family: int, s: State):
-        M, K = A_host.shape
+    def gemm_host(self, A_host, B_host, C_host, family: int, s: State, layout: int = LAYOUT_NN):
+        M, K = A_host.shape if layout == LAYOUT_NN else A_host.shape[::-1]
         _, N = B_host.shape
-        _check(lib.tt_gemm_host(self.h, M, N, K, family, A_host.data_ptr(), B_host.data_ptr(), C_host.data_ptr(),
-                                C.byref(to_config(s))), "gemm_host")
+        _check(lib.tt_gemm_host(self.h, M, N, K, family, layout, A_host.data_ptr(), B_host.data_ptr(),
+                                C_host.data_ptr(), C.byref(to_config(s))), "gemm_host")
 
 
 # ------------------------------------------------------------------------------------ searches

@@ -260,3 +260,32 @@ def test_bf16_exhaustive_vs_gbfs_4096():
     ctx.close()
     assert res.frac_raw <= 0.01
     assert res.best_cost <= best * 1.05, (res.best_cost, best)
+
+
+# ------------------------------------------------------------------ TN layout (P:372 Y = W^T X)
+@pytest.mark.parametrize("fam", [tt.FAM_F32_SIMT, tt.FAM_BF16_UMMA, tt.FAM_TF32_UMMA])
+def test_tn_layout_perceptron(fam):
+    # the paper's perceptron workload: W in R^(k x m), X in R^(k x n), Y = W^T X;
+    # (m, k, n) = (512, 256, 384) non-square so a swapped axis cannot pass
+    m, k, n = 512, 256, 384
+    bf16 = fam == tt.FAM_BF16_UMMA
+    W = synth.uniform_f32(synth.SEED_A, k, m)
+    X = synth.uniform_f32(synth.SEED_B, k, n)
+    if bf16:
+        W = synth.bf16_bits_to_f32(synth.to_bf16_bits(W))
+        X = synth.bf16_bits_to_f32(synth.to_bf16_bits(X))
+    A = np.ascontiguousarray(W.T)
+    R = og.gemm_f64(A, X)
+    sp = Spec(m, k, n, family=fam)
+    cfgs = [s for s in space.enumerate_configs(sp) if space.legitimate(sp, s)]
+    pick = [cfgs[i] for i in SplitMix64(5).sample_indices(len(cfgs), 12)]
+    Wd, Xd = to_dev(W, bf16), to_dev(X, bf16)
+    for s in pick:
+        C = torch.full((m, n), float("nan"), device=DEV)
+        tt.gemm(Wd, Xd, C, fam, s, layout=tt.LAYOUT_TN)
+        torch.cuda.synchronize()
+        Cn = C.cpu().numpy()
+        if fam == tt.FAM_F32_SIMT:
+            assert np.array_equal(Cn, og.gemm_fmaf(A, X)), s
+        else:
+            assert og.normwise_error(Cn, R) <= 5e-3, s
