@@ -277,6 +277,25 @@ tt_status tt_na2c_search(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, uint64_t 
                          const tt_search_opts* opts, tt_result* out, tt_trace_row* trace,
                          uint64_t trace_cap);
 
+/* ---------------------------------------------------------------- conv layer as a GEMM */
+
+/* im2col ("each depth-wise (channel) slice of input can be added into an input matrix as a
+ * row; similarly each kernel can be added into a kernel matrix as a column"): x is NCHW
+ * [Nb][C][H][W] (dtype 0 fp32, 1 bf16), A is written row-major [Nb*P*Q][C*R*S] with
+ * P = (H + 2 pad - R) / stride + 1, Q = (W + 2 pad - S) / stride + 1, row = (n P + p) Q + q,
+ * column = (c R + r) S + s; taps outside the image read 0.  Device pointers; async on stream. */
+tt_status tt_im2col(int32_t dtype, const void* x, int64_t Nb, int64_t C, int64_t H, int64_t W, int32_t R, int32_t S,
+                    int32_t stride, int32_t pad, void* A, void* stream);
+
+/* Conv layer y = conv(x, w) as im2col + the tiled GEMM of family `family`:
+ * y [Nb*P*Q][Kf] (fp32, i.e. NPQK) = im2col(x) [Nb*P*Q][C*R*S] . Wm, where Wm is the kernel matrix
+ * [C*R*S][Kf] (column kf = kernel kf flattened in (c, r, s) order).  cfg tiles the GEMM
+ * (M, N, K) = (Nb*P*Q, Kf, C*R*S).  workspace (device) holds the im2col matrix:
+ * workspace_bytes >= Nb*P*Q*C*R*S*elem, else TT_E_CAPACITY. */
+tt_status tt_conv2d(int32_t family, const void* x, int64_t Nb, int64_t C, int64_t H, int64_t W, const void* Wm,
+                    int64_t Kf, int32_t R, int32_t S, int32_t stride, int32_t pad, float* y, void* workspace,
+                    uint64_t workspace_bytes, const tt_config* cfg, void* stream);
+
 /* Random-search comparator ("configurations are randomly selected to be tested"):
  * the first budget_evals states of a uniform random permutation (SplitMix64 partial Fisher-Yates
  * with opts->seed) of the feasible set in rank order, measured in batches of opts->width.  Not the

@@ -66,3 +66,26 @@ void oracle_gemm_f64_entries(int64_t n, int64_t k, const double* A, const double
     out[t] = s;
   }
 }
+
+/* Direct convolution (cross-correlation, as in DL frameworks), the operation P:105 lowers to a GEMM:
+ * y[n][f][p][q] = sum_{c,r,s} x[n][c][p*st - pad + r][q*st - pad + s] * w[f][c][r][s], taps outside
+ * the image contribute 0.  Plain seven-deep loop in double, sequential over (c, r, s). */
+void oracle_conv2d_f64(int64_t Nb, int64_t C, int64_t H, int64_t W, int64_t F, int64_t R, int64_t S,
+                       int64_t st, int64_t pad, const double* x, const double* w, double* y) {
+  const int64_t P = (H + 2 * pad - R) / st + 1, Q = (W + 2 * pad - S) / st + 1;
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int64_t n = 0; n < Nb; ++n)
+    for (int64_t f = 0; f < F; ++f)
+      for (int64_t p = 0; p < P; ++p)
+        for (int64_t q = 0; q < Q; ++q) {
+          double acc = 0.0;
+          for (int64_t c = 0; c < C; ++c)
+            for (int64_t r = 0; r < R; ++r)
+              for (int64_t s = 0; s < S; ++s) {
+                const int64_t ih = p * st - pad + r, iw = q * st - pad + s;
+                if (ih < 0 || ih >= H || iw < 0 || iw >= W) continue;
+                acc += x[((n * C + c) * H + ih) * W + iw] * w[((f * C + c) * R + r) * S + s];
+              }
+          y[((n * F + f) * P + p) * Q + q] = acc;
+        }
+}

@@ -20,7 +20,7 @@ SRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "..", "build", "tiletune")
 LIB = os.path.join(HERE, "libtiletune.so")
 INCLUDE = os.path.join(HERE, "..", "include")
-SOURCES = ["space.cpp", "search.cpp", "abi.cpp", "ctx.cu", "gemm_simt.cu", "gemm_umma.cu"]
+SOURCES = ["space.cpp", "search.cpp", "abi.cpp", "ctx.cu", "gemm_simt.cu", "gemm_umma.cu", "conv.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

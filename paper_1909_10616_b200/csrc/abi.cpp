@@ -327,6 +327,33 @@ tt_status tt_gemm(int64_t M, int64_t N, int64_t K, int32_t family, const void* A
   return tt_gemm_ex(M, N, K, family, TT_LAYOUT_NN, A, B, C, cfg, stream);
 }
 
+tt_status tt_im2col(int32_t dtype, const void* x, int64_t Nb, int64_t C, int64_t H, int64_t W, int32_t R, int32_t S,
+                    int32_t stride, int32_t pad, void* A, void* stream) {
+  if (!x || !A) return fail(TT_E_INVAL, "null argument");
+  if (dtype != 0 && dtype != 1) return fail(TT_E_INVAL, "dtype must be 0 (fp32) or 1 (bf16)");
+  if (Nb < 1 || C < 1 || H < 1 || W < 1 || R < 1 || S < 1 || stride < 1 || pad < 0)
+    return fail(TT_E_INVAL, "bad convolution geometry");
+  std::string err;
+  tt_status r = launch_im2col(dtype, x, Nb, C, H, W, R, S, stride, pad, A, static_cast<cudaStream_t>(stream), &err);
+  return r == TT_OK ? TT_OK : fail(r, err);
+}
+
+tt_status tt_conv2d(int32_t family, const void* x, int64_t Nb, int64_t C, int64_t H, int64_t W, const void* Wm,
+                    int64_t Kf, int32_t R, int32_t S, int32_t stride, int32_t pad, float* y, void* workspace,
+                    uint64_t workspace_bytes, const tt_config* cfg, void* stream) {
+  if (!x || !Wm || !y || !workspace || !cfg) return fail(TT_E_INVAL, "null argument");
+  if (Nb < 1 || C < 1 || H < 1 || W < 1 || R < 1 || S < 1 || stride < 1 || pad < 0 || Kf < 1)
+    return fail(TT_E_INVAL, "bad convolution geometry");
+  const int64_t P = (H + 2 * pad - R) / stride + 1, Q = (W + 2 * pad - S) / stride + 1;
+  if (P < 1 || Q < 1) return fail(TT_E_INVAL, "empty convolution output");
+  const int64_t M = Nb * P * Q, K = C * (int64_t)R * S;
+  const uint64_t elem = family == TT_FAM_BF16_UMMA ? 2 : 4;
+  if (workspace_bytes < (uint64_t)M * K * elem) return fail(TT_E_CAPACITY, "workspace smaller than the im2col matrix");
+  tt_status r = tt_im2col(family == TT_FAM_BF16_UMMA ? 1 : 0, x, Nb, C, H, W, R, S, stride, pad, workspace, stream);
+  if (r != TT_OK) return r;
+  return tt_gemm_ex(M, Kf, K, family, TT_LAYOUT_NN, workspace, Wm, y, cfg, stream);
+}
+
 tt_status tt_ctx_create(int32_t device, uint64_t input_seed, tt_ctx** out) {
   if (!out) return fail(TT_E_INVAL, "null out");
   Ctx* c = new Ctx();

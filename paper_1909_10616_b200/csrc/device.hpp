@@ -21,6 +21,10 @@ tt_status launch_gemm(const Space& sp, const State& s, const void* A, const void
 tt_status launch_fill(void* dst, int dtype, uint64_t seed, uint64_t idx0, uint64_t count,
                       cudaStream_t stream, std::string* err);
 
+// K5: im2col for conv-as-GEMM.
+tt_status launch_im2col(int dtype, const void* x, int64_t Nb, int64_t C, int64_t H, int64_t W, int R, int S,
+                        int stride, int pad, void* A, cudaStream_t stream, std::string* err);
+
 // Family-specific launchers (gemm_simt.cu, gemm_umma.cu).
 tt_status simt_bind(const Space& sp, const State& s, tt_launch_info* info, std::string* err);
 tt_status simt_launch(const Space& sp, const State& s, const float* A, const float* B, float* C,

@@ -101,6 +101,8 @@ EXPORTS = {
                              C.POINTER(TraceRow), u64]),
     "tt_na2c_search": (i32, [vp, i64, i64, i64, u64, C.POINTER(SearchOpts), C.POINTER(Result),
                              C.POINTER(TraceRow), u64]),
+    "tt_im2col": (i32, [i32, vp, i64, i64, i64, i64, i32, i32, i32, i32, vp, vp]),
+    "tt_conv2d": (i32, [i32, vp, i64, i64, i64, i64, vp, i64, i32, i32, i32, i32, vp, vp, u64, C.POINTER(Config), vp]),
     "tt_random_search": (i32, [vp, i64, i64, i64, u64, C.POINTER(SearchOpts), C.POINTER(Result),
                                C.POINTER(TraceRow), u64]),
 }
@@ -387,3 +389,43 @@ def random_search(M: int, N: int, K: int, budget: int, opts: Optional[SearchOpts
                   ctx: Optional[Context] = None, **kw) -> SearchResult:
     """Random-search comparator.  Same contract as gbfs_search."""
     return _search(lib.tt_random_search, "random_search", M, N, K, budget, opts or search_opts(), ctx, **kw)
+
+
+# ------------------------------------------------------------------------------------ conv (P:105)
+def conv_out_hw(H, W, R, S, stride=1, pad=0):
+    return (H + 2 * pad - R) // stride + 1, (W + 2 * pad - S) // stride + 1
+
+
+def conv_gemm_dims(x_shape, Kf, R, S, stride=1, pad=0):
+    """(M, N, K) of the GEMM a conv layer becomes: (Nb*P*Q, Kf, C*R*S)."""
+    Nb, Cc, H, W = x_shape
+    P, Q = conv_out_hw(H, W, R, S, stride, pad)
+    return Nb * P * Q, Kf, Cc * R * S
+
+
+def im2col(x, R, S, stride=1, pad=0, out=None, stream=None):
+    """A [Nb*P*Q, C*R*S] from NCHW x (fp32 or bf16 CUDA tensor) on the device (tt_im2col)."""
+    import torch
+    Nb, Cc, H, W = x.shape
+    P, Q = conv_out_hw(H, W, R, S, stride, pad)
+    if out is None:
+        out = torch.empty(Nb * P * Q, Cc * R * S, device=x.device, dtype=x.dtype)
+    dt = {torch.float32: 0, torch.bfloat16: 1}[x.dtype]
+    _check(lib.tt_im2col(dt, x.data_ptr(), Nb, Cc, H, W, R, S, stride, pad, out.data_ptr(), _stream(stream)),
+           "im2col")
+    return out
+
+
+def conv2d(x, Wm, family: int, s: State, R: int, S: int, stride=1, pad=0, workspace=None, stream=None):
+    """Conv layer through im2col + the tiled GEMM: returns y [Nb*P*Q, Kf] fp32 (tt_conv2d);
+    Wm is the kernel matrix [C*R*S, Kf]."""
+    import torch
+    Nb, Cc, H, W = x.shape
+    M, Kf, K = conv_gemm_dims(x.shape, Wm.shape[1], R, S, stride, pad)
+    if workspace is None:
+        workspace = torch.empty(M * K, device=x.device, dtype=x.dtype)
+    y = torch.empty(M, Kf, device=x.device, dtype=torch.float32)
+    _check(lib.tt_conv2d(family, x.data_ptr(), Nb, Cc, H, W, Wm.data_ptr(), Kf, R, S, stride, pad, y.data_ptr(),
+                         workspace.data_ptr(), workspace.numel() * workspace.element_size(), C.byref(to_config(s)),
+                         _stream(stream)), "conv2d")
+    return y

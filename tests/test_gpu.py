@@ -289,3 +289,41 @@ def test_tn_layout_perceptron(fam):
             assert np.array_equal(Cn, og.gemm_fmaf(A, X)), s
         else:
             assert og.normwise_error(Cn, R) <= 5e-3, s
+
+
+# ------------------------------------------------------------------ conv layer as GEMM
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_im2col_bit_exact(dtype):
+    from oracle import conv
+    x = synth.uniform_f32(1, 2 * 3 * 9 * 10, 1).reshape(2, 3, 9, 10)
+    if dtype == "bf16":
+        x = synth.bf16_bits_to_f32(synth.to_bf16_bits(x))
+    xd = to_dev(x, dtype == "bf16")
+    for (R, S, st, pad) in [(3, 3, 1, 1), (5, 2, 2, 0), (1, 1, 1, 0)]:
+        A = tt.im2col(xd, R, S, st, pad)
+        torch.cuda.synchronize()
+        ref = conv.im2col_ref(x, R, S, st, pad)
+        assert np.array_equal(A.float().cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("fam", [tt.FAM_F32_SIMT, tt.FAM_BF16_UMMA, tt.FAM_TF32_UMMA])
+def test_conv2d_via_gemm(fam):
+    # a ResNet-style 3x3 layer: Nb=2, C=64, 16x16, F=128, pad 1 -> GEMM (M, N, K) = (512, 128, 576)
+    from oracle import conv
+    Nb, C, H, W, F, R, S = 2, 64, 16, 16, 128, 3, 3
+    bf16 = fam == tt.FAM_BF16_UMMA
+    x = synth.uniform_f32(1, Nb * C * H * W, 1).reshape(Nb, C, H, W)
+    w = synth.uniform_f32(2, F * C * R * S, 1).reshape(F, C, R, S)
+    if bf16:
+        x = synth.bf16_bits_to_f32(synth.to_bf16_bits(x))
+        w = synth.bf16_bits_to_f32(synth.to_bf16_bits(w))
+    M, N, K = tt.conv_gemm_dims(x.shape, F, R, S, 1, 1)
+    assert (M, N, K) == (512, 128, 576)
+    sp = Spec(M, K, N, family=fam)
+    s = hw.default_s0(sp) if fam != tt.FAM_F32_SIMT else ((4, 2, 8, 8), (72, 8), (1, 4, 4, 8))
+    assert space.legitimate(sp, s)
+    y = tt.conv2d(to_dev(x, bf16), to_dev(conv.kernel_matrix(w), bf16), fam, s, R, S, 1, 1)
+    torch.cuda.synchronize()
+    ref = conv.conv2d_f64(x, w, 1, 1)
+    got = y.cpu().numpy().reshape(Nb, H, W, F).transpose(0, 3, 1, 2)
+    assert og.normwise_error(got, ref) <= (1e-4 if fam == tt.FAM_F32_SIMT else 5e-3)
