@@ -32,6 +32,7 @@ struct SimtArgs {
   int m1, m2, n1, n2, bk, k0;
   int bk_sh;  // log2(BK) if BK is a power of two, else -1
   int bq_sh;  // log2(BN / 4) if a power of two, else -1
+  int stages; // shared-memory slots (2 or 3)
   int a_tn;   // A stored as W = A^T row-major [K][M] (the paper's Y = W^T X)
   int a_vec16;  // TN: 16-byte cp.async of W rows legal
   int b_vec;  // B rows 16-byte aligned (16-byte cp.async legal)
@@ -108,8 +109,9 @@ k1_simt(SimtArgs p) {
   const int BN = p.n1 * p.n2 * TN;
   const int BK = p.bk;
   const int LDA = BM + 4, LDB = BN + 4;
-  float* Bs = smem;                      // [2][BK][LDB]
-  float* As = smem + 2 * BK * LDB;       // [2][BK][LDA]
+  const int NS = p.stages;               // 2 or 3 smem slots (binder: 3 when occupancy allows)
+  float* Bs = smem;                      // [NS][BK][LDB]
+  float* As = smem + NS * BK * LDB;      // [NS][BK][LDA]
 
   const int T = blockDim.x;
   const int t = threadIdx.x;
@@ -193,17 +195,19 @@ k1_simt(SimtArgs p) {
     }
   }
 
-  load(0, 0);
-  cp_async_commit();
+  // prologue: slots 0 .. NS-2 in flight; every iteration commits one group (possibly empty) so
+  // wait_group<NS-1> always means "tile kt has landed"
+  for (int pk = 0; pk < NS - 1; ++pk) {
+    if (pk < p.k0) load(pk, pk);
+    cp_async_commit();
+  }
+  int buf = 0;
   for (int kt = 0; kt < p.k0; ++kt) {
-    const int buf = kt & 1;
-    if (kt + 1 < p.k0) {
-      load(kt + 1, buf ^ 1);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    const int nxt = kt + NS - 1;
+    if (nxt < p.k0) load(nxt, nxt % NS);
+    cp_async_commit();
+    if (NS == 3) cp_async_wait<2>();
+    else cp_async_wait<1>();
     __syncthreads();
     const float* as = As + buf * BK * LDA + row0;
     const float* bs = Bs + buf * BK * LDB + col0;
@@ -218,6 +222,7 @@ k1_simt(SimtArgs p) {
       fma_frag<TM, TN, kPair>(a1, b1, acc, acc2);
     }
     if (kk < BK) fma_frag<TM, TN, kPair>(a0, b0, acc, acc2);   // odd BK: last step
+    if (++buf == NS) buf = 0;
     __syncthreads();
   }
   if constexpr (kPair) {
@@ -292,8 +297,12 @@ tt_status simt_bind(const Space& sp, const State& s, tt_launch_info* info, std::
   info->grid_z = 1;
   info->block_x = (int32_t)(m1 * n1 * m2 * n2);
   info->cluster_x = 1;
-  info->smem_bytes = (int32_t)(kSimtStages * (m1 * m2 * m3 + n1 * n2 * n3 + 2 * kSimtPad) * k1 * 4);
-  info->stages = kSimtStages;
+  // J_hw guarantees 2 slots fit.  The kernel also runs 3 slots, but measured no faster on B200
+  // (2048^3: 40.7 vs 42.3 TF/s, 4096^3: 47.7 vs 49.3), so the binder keeps 2.
+  const int64_t slot = (m1 * m2 * m3 + n1 * n2 * n3 + 2 * kSimtPad) * k1 * 4;
+  const int stages = kSimtStages;
+  info->smem_bytes = (int32_t)(stages * slot);
+  info->stages = stages;
   info->tile_m = (int32_t)(m1 * m2 * m3);
   info->tile_n = (int32_t)(n1 * n2 * n3);
   info->tile_k = (int32_t)k1;
@@ -341,6 +350,7 @@ tt_status simt_launch(const Space& sp, const State& s, const float* A, const flo
   a.bq_sh = (li.tile_n % 4 == 0) ? lg(li.tile_n / 4) : -1;
   a.b_vec = (li.tile_n % 4 == 0 && a.N % 4 == 0 && ((uintptr_t)B % 16) == 0) ? 1 : 0;
   a.a_tn = sp.layout == TT_LAYOUT_TN ? 1 : 0;
+  a.stages = li.stages;
   a.a_vec16 = (li.tile_m % 4 == 0 && a.M % 4 == 0 && ((uintptr_t)A % 16) == 0 &&
                ((2 * (int64_t)a.bk * (li.tile_n + 4)) % 4) == 0) ? 1 : 0;
   dim3 grid((unsigned)li.grid_x, (unsigned)li.grid_y, 1);
