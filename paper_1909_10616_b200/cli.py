@@ -135,8 +135,38 @@ def _run(strategy, args, seed, ctx):
         opts.has_s0 = 1
         opts.s0 = tt.to_config(decode(args.start_config, (args.dm, args.dk, args.dn)))
     fn = {"gbfs": tt.gbfs_search, "na2c": tt.na2c_search, "random": tt.random_search}[strategy]
-    kw = {"ctx": ctx} if args.backend == "device" else {"cost": synthetic_cost(args)}
-    return fn(args.m, args.n, args.k, args.max_evals, opts, **kw)
+    recorded = _load_resume(args, strategy, seed)
+    if recorded is None:
+        kw = {"ctx": ctx} if args.backend == "device" else {"cost": synthetic_cost(args)}
+        return fn(args.m, args.n, args.k, args.max_evals, opts, **kw)
+    # Resume (SURVEY §5 checkpoint): a search is a deterministic function of (seed, cost sequence),
+    # so replaying the recorded costs rebuilds Q / S_v / H_v / the RNG state exactly and the search
+    # continues live once it reaches states the trace does not hold.
+    sp = _space(args)
+    live = synthetic_cost(args) if args.backend == "synthetic" else None
+
+    def batch(states):
+        out = []
+        for s in states:
+            if s in recorded:
+                out.append(recorded[s])
+            elif live is not None:
+                out.append(live(s))
+            else:
+                out.append(ctx.measure(sp, s, tt.measure_opts(repeats=args.repeats, warmup=args.warmup)).cost_s)
+        return out
+    return fn(args.m, args.n, args.k, args.max_evals, opts, batch=batch)
+
+
+def _load_resume(args, strategy, seed):
+    if not getattr(args, "resume", None):
+        return None
+    rec = {}
+    with open(args.resume, newline="") as f:
+        for r in csv.DictReader(f):
+            if r["strategy"] == strategy and int(r["trial_seed"]) == seed:
+                rec[decode(r["config"], (args.dm, args.dk, args.dn))] = float(r["cost_s"])
+    return rec
 
 
 def _tune(args, strategies):
@@ -236,6 +266,7 @@ def main(argv=None):
         p.add_argument("--warmup", type=int, default=2)
         p.add_argument("--start-config", default=None)
         p.add_argument("--out", default="runs/tune")
+        p.add_argument("--resume", default=None, help="CSV trace of an earlier run: replay it, then continue")
         p.set_defaults(fn=fn)
     args = ap.parse_args(argv)
     args.fn(args)

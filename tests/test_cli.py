@@ -62,3 +62,15 @@ def test_compare_refuses_single_strategy(tmp_path):
                         "64", "--backend", "synthetic", "--strategies", "gbfs", "--out", str(tmp_path / "x")],
                        capture_output=True, text=True)
     assert r.returncode != 0
+
+
+def test_resume_from_trace_is_exact(tmp_path):
+    # the trace is the checkpoint.  A 120-eval run resumed to 250 == a direct 250 run.
+    base = ["tune", "--m", "64", "--k", "64", "--n", "64", "--backend", "synthetic", "--seeds", "3"]
+    for strat in ("gbfs", "na2c", "random"):
+        a, b, c = (str(tmp_path / f"{strat}_{x}") for x in "abc")
+        run(*base, "--strategy", strat, "--max-evals", "120", "--out", a)
+        run(*base, "--strategy", strat, "--max-evals", "250", "--resume", a + ".csv", "--out", b)
+        run(*base, "--strategy", strat, "--max-evals", "250", "--out", c)
+        key = lambda p: [(r["eval_index"], r["config"], r["cost_s"]) for r in csv.DictReader(open(p + ".csv"))]
+        assert key(b) == key(c) and len(key(b)) == 250

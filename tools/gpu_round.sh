@@ -3,7 +3,7 @@
 # the bench's dominant kernel.  Outputs under gpurun_out/ (scratch); summaries are copied into
 # profiles/ by tools/summarize_profiles.py on the CPU side.
 set -u
-TAG=${1:-r1}
+TAG=${1:-r2}
 OUT=gpurun_out
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu_$TAG.txt 2>&1
