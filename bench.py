@@ -245,10 +245,20 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TT_BENCH_SHARE_GPU=1: every rank on cuda:0 with gloo collectives -- exercises the N > 1 code
+    # path (sharded tuning, row partition, max-over-ranks) on a one-GPU box; its timings are not
+    # a scaling measurement (the ranks share one device).
+    share = os.environ.get("TT_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    coll = torch.device("cpu") if share else dev     # device of the small collective tensors
 
     Mr, N, K, fam, default_budget = WORKLOADS[args.workload]
     strong = args.workload == "bf16_8192"
@@ -269,12 +279,12 @@ def main():
         tune = None
     else:
         measure_one, observe = tdist.device_measure(ctx, sp)
-        ev = tdist.TrackingEvaluator(measure_one, observe, device=dev if world > 1 else None)
+        ev = tdist.TrackingEvaluator(measure_one, observe, device=coll if world > 1 else None)
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         res = tt.gbfs_search(Mr, N, K, budget, tt.search_opts(family=fam, seed=args.seed, width=args.width, layout=layout), batch=ev)
-        tune_wall = tdist.max_over_ranks(time.perf_counter() - t0, dev)
+        tune_wall = tdist.max_over_ranks(time.perf_counter() - t0, coll)
         best = res.best
         tune = {"algorithm": "G-BFS (Alg. 1, width %d, rho 5)" % args.width, "budget": budget, "evals": res.evals,
                 "space_raw": raw, "space_feasible": feasible, "frac_raw": res.frac_raw,
@@ -318,7 +328,7 @@ def main():
     clocks = sampler.stop()
     per = [s.elapsed_time(e) for s, e in zip(starts, ends)]       # ms, launching stream
     ms_local = sum(per) / len(per)
-    ms = tdist.max_over_ranks(ms_local, dev)
+    ms = tdist.max_over_ranks(ms_local, coll)
     flops_rank = 2.0 * Mr * N * K
     value = world * flops_rank / (ms * 1e-3) / 1e12                 # whole-job TFLOP/s
 
@@ -355,7 +365,7 @@ def main():
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         ctx.gemm_host(Ah_t, Bh_t, Ch_t, fam, best, layout=layout)
-    e2e_s = tdist.max_over_ranks((time.perf_counter() - t0) / e2e_steps, dev)
+    e2e_s = tdist.max_over_ranks((time.perf_counter() - t0) / e2e_steps, coll)
     e2e_val = world * flops_rank / e2e_s / 1e12
     h2d = Ah_t.numel() * Ah_t.element_size() + Bh_t.numel() * Bh_t.element_size()
     d2h = Ch_t.numel() * 4
@@ -397,7 +407,7 @@ def main():
             "config": {"workload": args.workload, "M_per_rank": Mr, "M_total": M, "N": N, "K": K,
                        "layout": args.layout,
                        "family": {1: "f32_simt", 2: "tf32_umma", 3: "bf16_umma"}[fam],
-                       "parallelism": f"row-partitioned x{world}, candidate sharding x{world}",
+                       "parallelism": f"row-partitioned x{world}, candidate sharding x{world}" + (" (shared GPU, gloo: code-path check)" if share else ""),
                        "l2": "flushed (256 MiB memset) before every timed launch",
                        "best_config": {"m": list(best[0]), "k": list(best[1]), "n": list(best[2])},
                        "launch": {"grid": info.grid_x, "cluster": info.cluster_x, "tile": [info.tile_m, info.tile_n,

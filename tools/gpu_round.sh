@@ -18,3 +18,7 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_um
     python bench.py --config "$CFG" --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_$TAG.log 2>&1
 timeout 300 python bench.py --impl reference --steps 5 --warmup 3 > $OUT/bench_ref_$TAG.json 2>&1
 ls -la $OUT
+# N > 1 code path on one GPU (gloo, shared device): must print one JSON line and exit 0
+TT_BENCH_SHARE_GPU=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+    --master-port 29517 bench.py --gpus 2 --steps 5 --warmup 3 > $OUT/bench_n2share_$TAG.json 2> $OUT/bench_n2share_$TAG.err
+echo "n2 shared rc=$?" >> $OUT/bench_n2share_$TAG.err
