@@ -42,6 +42,8 @@ WORKLOADS = {
     # BASELINE configs[4]: 8192^3 row-partitioned; M per rank = 8192 / N GPUs (strong scaling)
     "bf16_8192": (8192, 8192, 8192, 3, 64),
     "tf32_2048": (2048, 2048, 2048, 2, 64),
+    "tf32_4096": (4096, 4096, 4096, 2, 64),
+    "f32_4096": (4096, 4096, 4096, 1, 256),
     "f32_2048": (2048, 2048, 2048, 1, 256),
     "f32_512": (512, 512, 512, 1, 484),
 }
