@@ -256,8 +256,10 @@ tt_status tt_ctx_operands(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, int32_t 
                           const void** A, const void** B, float** C);
 
 /* cost(s) on hardware ("test (i.e., run the configuration on target hardware)"):
- * warmup, one probe, then R repeats of `number` launches between CUDA events on the ctx stream;
- * cost = median of per-repeat means (Z10).  TT_E_ILLEGITIMATE / TT_E_INFEASIBLE for a config
+ * one cold timed probe (if it exceeds opts->cut_s the candidate is scored by it, Z12), warmup
+ * launches, a warm probe that sizes `number`, then R repeats of `number` launches between CUDA
+ * events on the ctx stream; cost = median of per-repeat means (Z10).  The measured operands are
+ * the ctx's (K4 recipe); the space's layout selects the NN or TN kernel.  TT_E_ILLEGITIMATE / TT_E_INFEASIBLE for a config
  * without J; TT_E_CUDA on a launch error. */
 tt_status tt_measure(tt_ctx* ctx, const tt_space* sp, const tt_config* cfg,
                      const tt_measure_opts* opts, tt_sample* out);
