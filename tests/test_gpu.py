@@ -327,3 +327,25 @@ def test_conv2d_via_gemm(fam):
     ref = conv.conv2d_f64(x, w, 1, 1)
     got = y.cpu().numpy().reshape(Nb, H, W, F).transpose(0, 3, 1, 2)
     assert og.normwise_error(got, ref) <= (1e-4 if fam == tt.FAM_F32_SIMT else 5e-3)
+
+
+@pytest.mark.parametrize("M,N,K,s", [
+    (8192, 8192, 8192, ((16, 2, 2, 128), (128, 64), (32, 1, 1, 256))),     # bench bf16_8192 config
+    (1024, 8192, 8192, ((4, 2, 1, 128), (128, 64), (32, 1, 1, 256))),      # C5 shard at 8 GPUs
+])
+def test_bf16_max_sizes_sampled(M, N, K, s):
+    # BASELINE configs[4] sizes, in the launch configuration bench.py times; sampled entries
+    Ab = synth.to_bf16_bits(synth.uniform_f32(synth.SEED_A, M, K))
+    Bb = synth.to_bf16_bits(synth.uniform_f32(synth.SEED_B, K, N))
+    Ad = torch.from_numpy(Ab.view(np.int16)).to(DEV).view(torch.bfloat16)
+    Bd = torch.from_numpy(Bb.view(np.int16)).to(DEV).view(torch.bfloat16)
+    C = torch.full((M, N), float("nan"), device=DEV)
+    tt.gemm(Ad, Bd, C, tt.FAM_BF16_UMMA, s)
+    torch.cuda.synchronize()
+    assert not torch.isnan(C).any()
+    rng = np.random.default_rng(0)
+    ii, jj = rng.integers(0, M, 512), rng.integers(0, N, 512)
+    A32, B32 = synth.bf16_bits_to_f32(Ab), synth.bf16_bits_to_f32(Bb)
+    R = og.gemm_f64_entries(A32, B32, ii, jj)
+    got = C[torch.from_numpy(ii).to(DEV), torch.from_numpy(jj).to(DEV)].cpu().numpy()
+    assert og.normwise_error(got, R) <= 5e-3
