@@ -77,6 +77,15 @@ Ctx::~Ctx() {
   cudaFree(hB);
   cudaFree(hC);
   for (auto e : ev) cudaEventDestroy(e);
+  if (s_in) {
+    cudaEventDestroy(e_b);
+    for (int i = 0; i < 8; ++i) {
+      cudaEventDestroy(e_in[i]);
+      cudaEventDestroy(e_c[i]);
+    }
+    cudaStreamDestroy(s_in);
+    cudaStreamDestroy(s_out);
+  }
   if (stream) cudaStreamDestroy(stream);
   cudaSetDevice(prev);
 }
@@ -222,12 +231,49 @@ tt_status Ctx::gemm_host(const Space& sp, const State& s, const void* Ah, const 
     return true;
   };
   if (!grow(&hA, &hAcap, a) || !grow(&hB, &hBcap, b) || !grow(&hC, &hCcap, c)) return TT_E_CUDA;
-  if (!cuda_ok(cudaMemcpyAsync(hA, Ah, a, cudaMemcpyHostToDevice, stream), err, "H2D A")) return TT_E_CUDA;
-  if (!cuda_ok(cudaMemcpyAsync(hB, Bh, b, cudaMemcpyHostToDevice, stream), err, "H2D B")) return TT_E_CUDA;
-  tt_status st = launch_gemm(sp, s, hA, hB, static_cast<float*>(hC), stream, err);
-  if (st != TT_OK) return st;
-  if (!cuda_ok(cudaMemcpyAsync(Ch, hC, c, cudaMemcpyDeviceToHost, stream), err, "D2H C")) return TT_E_CUDA;
-  return cuda_ok(cudaStreamSynchronize(stream), err, "gemm_host sync") ? TT_OK : TT_E_CUDA;
+  if (!s_in) {
+    if (!cuda_ok(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking), err, "stream") ||
+        !cuda_ok(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking), err, "stream"))
+      return TT_E_CUDA;
+    for (auto* e : {&e_b, &e_in[0], &e_in[1], &e_in[2], &e_in[3], &e_in[4], &e_in[5], &e_in[6], &e_in[7], &e_c[0],
+                    &e_c[1], &e_c[2], &e_c[3], &e_c[4], &e_c[5], &e_c[6], &e_c[7]})
+      if (!cuda_ok(cudaEventCreateWithFlags(e, cudaEventDisableTiming), err, "event")) return TT_E_CUDA;
+  }
+  // Row-chunked pipeline (NN layout): B, then A chunk i, on the copy-in stream; GEMM of chunk i
+  // (the same tiles, m0 / chunks of them) once A_i has landed; D2H of C_i on the copy-out stream
+  // as soon as it is computed -- the two PCIe directions and the GEMM overlap.
+  const int64_t m0 = s.f[0][0];
+  int chunks = 1;
+  if (sp.layout == TT_LAYOUT_NN)
+    for (int c2 : {8, 4, 2})
+      if (m0 % c2 == 0) { chunks = c2; break; }
+  const int64_t Mc = sp.dim[0] / chunks;
+  const size_t ac = (size_t)Mc * sp.dim[1] * es, cc = (size_t)Mc * sp.dim[2] * 4;
+  tt_space sub{Mc, sp.dim[2], sp.dim[1], sp.d[0], sp.d[1], sp.d[2], sp.family, sp.layout};
+  Space sps(sub, false);
+  State sc = s;
+  sc.f[0][0] = m0 / chunks;
+  if (!cuda_ok(cudaMemcpyAsync(hB, Bh, b, cudaMemcpyHostToDevice, s_in), err, "H2D B")) return TT_E_CUDA;
+  cudaEventRecord(e_b, s_in);
+  cudaStreamWaitEvent(stream, e_b, 0);
+  for (int i = 0; i < chunks; ++i) {
+    char* dA = static_cast<char*>(hA) + (size_t)i * ac;
+    if (!cuda_ok(cudaMemcpyAsync(dA, static_cast<const char*>(Ah) + (size_t)i * ac, ac, cudaMemcpyHostToDevice, s_in),
+                 err, "H2D A"))
+      return TT_E_CUDA;
+    cudaEventRecord(e_in[i], s_in);
+    cudaStreamWaitEvent(stream, e_in[i], 0);
+    float* dC = reinterpret_cast<float*>(static_cast<char*>(hC) + (size_t)i * cc);
+    tt_status st = launch_gemm(chunks == 1 ? sp : sps, chunks == 1 ? s : sc, dA, hB, dC, stream, err);
+    if (st != TT_OK) return st;
+    cudaEventRecord(e_c[i], stream);
+    cudaStreamWaitEvent(s_out, e_c[i], 0);
+    if (!cuda_ok(cudaMemcpyAsync(reinterpret_cast<char*>(Ch) + (size_t)i * cc, dC, cc, cudaMemcpyDeviceToHost, s_out),
+                 err, "D2H C"))
+      return TT_E_CUDA;
+  }
+  (void)c;
+  return cuda_ok(cudaStreamSynchronize(s_out), err, "gemm_host sync") ? TT_OK : TT_E_CUDA;
 }
 
 }  // namespace tt

@@ -33,6 +33,8 @@ struct Ctx : tt_ctx {
   uint64_t flush_gen = 0;
   void *hA = nullptr, *hB = nullptr, *hC = nullptr;
   size_t hAcap = 0, hBcap = 0, hCcap = 0;
+  cudaStream_t s_in = nullptr, s_out = nullptr;   // gemm_host copy streams (H2D, D2H)
+  cudaEvent_t e_b = nullptr, e_in[8] = {}, e_c[8] = {};
 
   ~Ctx();
   tt_status init(std::string* err);
