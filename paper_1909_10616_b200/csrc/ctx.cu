@@ -16,6 +16,7 @@
 
 #include "ctx.hpp"
 #include "device.hpp"
+#include "trace.hpp"
 
 namespace tt {
 
@@ -145,6 +146,7 @@ tt_status Ctx::flush_l2(std::string* err) {
 
 tt_status Ctx::measure(const Space& sp, const State& s, const tt_measure_opts& mo, tt_sample* out,
                        std::string* err) {
+  NvtxRange nv("tt_measure");
   Operands* o = nullptr;
   tt_status st = operands(sp, &o, err);
   if (st != TT_OK) return st;
@@ -217,6 +219,7 @@ tt_status Ctx::measure(const Space& sp, const State& s, const tt_measure_opts& m
 
 tt_status Ctx::gemm_host(const Space& sp, const State& s, const void* Ah, const void* Bh, float* Ch,
                          std::string* err) {
+  NvtxRange nv("tt_gemm_host");
   const size_t es = sp.family == TT_FAM_BF16_UMMA ? 2 : 4;
   const size_t a = (size_t)sp.dim[0] * sp.dim[1] * es, b = (size_t)sp.dim[1] * sp.dim[2] * es,
                c = (size_t)sp.dim[0] * sp.dim[2] * 4;

@@ -2,6 +2,7 @@
 // MDP of Sec. "Configuration Search Modeling".  Readings Z4-Z9 (G-BFS) and Z18
 // (N-A2C) are listed in DESIGN.md §3; the RNG is SplitMix64 (O7).
 #include "search.hpp"
+#include "trace.hpp"
 
 #include <chrono>
 #include <cmath>
@@ -95,6 +96,7 @@ tt_status gbfs_search(const Space& sp, const State& s0, uint64_t budget, const t
   tt_status result = TT_OK;
   while (!q.empty() && evals < budget) {                                               // line 4
     if (o.budget_seconds > 0 && now_s() - t0 >= o.budget_seconds) break;
+    NvtxRange nv("gbfs round");
     popped.clear();
     for (int w = 0; w < width && !q.empty(); ++w) {                                   // line 5 (Z9)
       popped.push_back(q.top().s);
@@ -310,6 +312,7 @@ tt_status na2c_search(const Space& sp, const State& s0, uint64_t budget, const t
     const int Te = o.steps_T_decay_every > 0 ? (int)std::max<int64_t>(Tfloor, T0 - episode / o.steps_T_decay_every) : T0;
     ++episode;
     int T = Te;
+    NvtxRange nv("na2c episode");
     std::vector<State> coll;
     std::unordered_set<uint64_t> cset;
     bool exhausted = false;
