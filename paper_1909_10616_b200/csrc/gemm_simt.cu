@@ -35,6 +35,7 @@ struct SimtArgs {
   int stages; // shared-memory slots (2 or 3)
   int a_tn;   // A stored as W = A^T row-major [K][M] (the paper's Y = W^T X)
   int a_vec16;  // TN: 16-byte cp.async of W rows legal
+  int c_vec;    // C rows 16-byte aligned (STG.128 legal)
   int b_vec;  // B rows 16-byte aligned (16-byte cp.async legal)
 };
 
@@ -239,7 +240,7 @@ k1_simt(SimtArgs p) {
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
     if constexpr (TN % 4 == 0) {
-      if ((N & 3) == 0) {
+      if (p.c_vec) {
 #pragma unroll
         for (int j = 0; j < TN; j += 4)
           *reinterpret_cast<float4*>(Cb + i * N + j) = make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
@@ -350,6 +351,7 @@ tt_status simt_launch(const Space& sp, const State& s, const float* A, const flo
   a.bq_sh = (li.tile_n % 4 == 0) ? lg(li.tile_n / 4) : -1;
   a.b_vec = (li.tile_n % 4 == 0 && a.N % 4 == 0 && ((uintptr_t)B % 16) == 0) ? 1 : 0;
   a.a_tn = sp.layout == TT_LAYOUT_TN ? 1 : 0;
+  a.c_vec = (a.N % 4 == 0 && ((uintptr_t)C % 16) == 0) ? 1 : 0;
   a.stages = li.stages;
   a.a_vec16 = (li.tile_m % 4 == 0 && a.M % 4 == 0 && ((uintptr_t)A % 16) == 0 &&
                ((2 * (int64_t)a.bk * (li.tile_n + 4)) % 4) == 0) ? 1 : 0;

@@ -349,3 +349,21 @@ def test_bf16_max_sizes_sampled(M, N, K, s):
     R = og.gemm_f64_entries(A32, B32, ii, jj)
     got = C[torch.from_numpy(ii).to(DEV), torch.from_numpy(jj).to(DEV)].cpu().numpy()
     assert og.normwise_error(got, R) <= 5e-3
+
+
+def test_simt_unaligned_views():
+    # views whose data pointer is only 4-byte aligned take the scalar load/store paths
+    M, N, K = 64, 64, 32
+    A, B = host_inputs(M, N, K)
+    Abuf = torch.zeros(M * K + 1, device=DEV)
+    Bbuf = torch.zeros(K * N + 1, device=DEV)
+    Cbuf = torch.full((M * N + 1,), float("nan"), device=DEV)
+    Abuf[1:].copy_(torch.from_numpy(A).reshape(-1))
+    Bbuf[1:].copy_(torch.from_numpy(B).reshape(-1))
+    Av, Bv, Cv = Abuf[1:].view(M, K), Bbuf[1:].view(K, N), Cbuf[1:].view(M, N)
+    tt.gemm(Av, Bv, Cv, tt.FAM_F32_SIMT, ((2, 2, 4, 4), (4, 8), (2, 2, 4, 4)))
+    torch.cuda.synchronize()
+    assert np.array_equal(Cv.cpu().numpy(), og.gemm_fmaf(A, B))
+    with pytest.raises(tt.TileTuneError):
+        tt.gemm(to_dev(A, True)[:, :].contiguous(), Bbuf[1:].view(K, N).to(torch.bfloat16), torch.empty(M, N, device=DEV),
+                tt.FAM_BF16_UMMA, ((1, 1, 1, 128), (2, 16), (1, 1, 1, 64)))
