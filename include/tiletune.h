@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define TT_VERSION 2
+#define TT_VERSION 3
 #define TT_MAXD 4  /* maximum loop depth per axis carried in tt_config */
 
 typedef enum {
@@ -168,6 +168,10 @@ typedef struct {
   int32_t acc_buffers;     /* UMMA: TMEM accumulator buffers */
   uint32_t idesc;          /* UMMA: instruction descriptor */
   int32_t reg_tile_m, reg_tile_n;   /* SIMT: per-thread register tile m3 x n3 */
+  /* UMMA tail split: when the tile count is not a multiple of the co-resident
+   * clusters, the last split_tiles tiles' k-blocks are shared by split_workers clusters (<= 4 per
+   * tile) and combined in descending-k order (store, then TMA reduce-adds); 0 = none. */
+  int32_t split_tiles, split_workers;
 } tt_launch_info;
 
 typedef struct tt_ctx tt_ctx;

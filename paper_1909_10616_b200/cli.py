@@ -192,14 +192,18 @@ def _tune(args, strategies):
         if args.backend == "device":
             st["best_tflops"] = box([flops / c / 1e12 for c in bests])
         summary["strategies"][strat] = st
-    with open(args.out + ".csv", "w", newline="") as f:
+        _write_outputs(args.out, rows, summary)     # after every strategy: a cut-off run keeps its finished part
+    print(json.dumps(summary["strategies"], indent=1))
+
+
+def _write_outputs(out, rows, summary):
+    with open(out + ".csv", "w", newline="") as f:
         w = csv.writer(f)
         w.writerow(["strategy", "trial_seed", "eval_index", "wall_clock_s", "config", "cost_s", "best_so_far_s",
                     "fraction_explored"])
         w.writerows(rows)
-    with open(args.out + ".json", "w") as f:
+    with open(out + ".json", "w") as f:
         json.dump(summary, f, indent=1)
-    print(json.dumps(summary["strategies"], indent=1))
 
 
 def cmd_tune(args):

@@ -20,7 +20,9 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 
 #include "device.hpp"
 
@@ -47,6 +49,10 @@ struct UmmaArgs {
   int a_stage_bytes, stage_bytes;   // A part, total per stage (A + padded B)
   uint32_t idesc;
   uint32_t tx_bytes;                // bytes landing per stage per CTA
+  // tail split: the last sk_tiles tiles' k-blocks are spread evenly over the
+  // first sk_workers clusters; the remaining dp_tiles tiles go round-robin to all clusters.
+  int dp_tiles, sk_tiles, sk_workers;
+  uint32_t* flags;                  // per split tile and CTA rank: completed-writer count x 4
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -96,6 +102,30 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int x, int y) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
                ::"l"(map), "r"(x), "r"(y), "r"(src) : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, uint32_t src, int x, int y) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];"
+               ::"l"(map), "r"(x), "r"(y), "r"(src) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t atom_add_release(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.release.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+// Spin until *flag >= target (written by the co-resident cluster that owns the higher k-blocks
+// of the same tile); the watchdog turns a lost writer into a trap instead of a hang.
+__device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target) {
+  if (ld_acquire(flag) >= target) return;
+  const uint64_t t0 = globaltimer();
+  while (ld_acquire(flag) < target) {
+    if (globaltimer() - t0 > 10000000000ull) __trap();
+  }
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
@@ -199,9 +229,62 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 template <int KIND>
 __device__ __forceinline__ constexpr uint32_t kind_sbo_mn() { return KIND == 1 ? 4u * 128u : 8u * 128u; }
 
+// One unit of work for a cluster: k-blocks [kb0, kb1) of output tile `tile`.  A split tile's
+// partial sums are combined in descending-k order: the piece holding the last k-block (order 0)
+// stores C, each lower piece waits until the pieces above it have landed and adds with a TMA
+// reduce.  Every role warp walks the identical sequence.
+struct Item {
+  int tile, kb0, kb1, order;
+  bool split;
+};
+
+struct Sched {
+  int w, P, dp;
+  int64_t pos, end;
+  __device__ __forceinline__ static int64_t sk_begin(const UmmaArgs& p, int v) {
+    return (int64_t)v * ((int64_t)p.sk_tiles * p.k0) / p.sk_workers;
+  }
+  __device__ __forceinline__ Sched(const UmmaArgs& p, int w_, int P_) : w(w_), P(P_), dp(w_), pos(0), end(0) {
+    if (w < p.sk_workers) {
+      pos = sk_begin(p, w);
+      end = sk_begin(p, w + 1);
+    }
+  }
+  // tail pieces first (their cross-cluster waits resolve while the data-parallel tiles run)
+  __device__ __forceinline__ bool next(const UmmaArgs& p, Item* it) {
+    if (pos < end) {
+      const int64_t t_rel = pos / p.k0;
+      const int kb0 = (int)(pos - t_rel * p.k0);
+      const int kb1 = (int)min((int64_t)p.k0, (int64_t)kb0 + (end - pos));
+      it->tile = p.dp_tiles + (int)t_rel;
+      it->kb0 = kb0;
+      it->kb1 = kb1;
+      it->split = !(kb0 == 0 && kb1 == p.k0);
+      int order = 0;
+      if (it->split) {
+        const int64_t tend = (t_rel + 1) * p.k0;
+        for (int v = w + 1; v < p.sk_workers; ++v) {
+          const int64_t b = sk_begin(p, v);
+          if (b >= tend) break;
+          if (sk_begin(p, v + 1) > b) ++order;
+        }
+      }
+      it->order = order;
+      pos += kb1 - kb0;
+      return true;
+    }
+    if (dp < p.dp_tiles) {
+      *it = Item{dp, 0, p.k0, 0, false};
+      dp += P;
+      return true;
+    }
+    return false;
+  }
+};
+
 struct MmaCtx {
   uint32_t sbase, full0, empty0, tfull0, tempty0, tmem_base;
-  int cluster_id, num_clusters, num_tiles;
+  int cluster_id, num_clusters;
 };
 
 template <int KIND, int CG, int KS, int M2, int N2>
@@ -239,11 +322,13 @@ __device__ __forceinline__ void mma_role(const UmmaArgs& p, const MmaCtx& c) {
   uint32_t phase = 0;
   int acc = 0;
   uint32_t aphase = 0;
-  for (int tile = c.cluster_id; tile < c.num_tiles; tile += c.num_clusters) {
+  Sched sch(p, c.cluster_id, c.num_clusters);
+  Item it;
+  while (sch.next(p, &it)) {
     mbar_wait(c.tempty0 + 8u * acc, aphase ^ 1u);
     tc_fence_after();
     const uint32_t dbase = c.tmem_base + (uint32_t)(acc * p.acc_cols);
-    for (int kb = 0; kb < p.k0; ++kb) {
+    for (int kb = it.kb0; kb < it.kb1; ++kb) {
       mbar_wait(c.full0 + 8u * stage, phase);
       tc_fence_after();
       const uint32_t sa16 = (c.sbase + (uint32_t)stage * p.stage_bytes) >> 4;
@@ -256,7 +341,7 @@ __device__ __forceinline__ void mma_role(const UmmaArgs& p, const MmaCtx& c) {
 #pragma unroll
             for (int ni = 0; ni < N2; ++ni)
               umma<KIND, CG>(dbase + d_off[mi][ni], a_hi | (uint64_t)(sa16 + a_off[ks][mi]),
-                             b_hi | (uint64_t)(sb16 + b_off[ks][ni]), p.idesc, (kb | ks) != 0 ? 1u : 0u);
+                             b_hi | (uint64_t)(sb16 + b_off[ks][ni]), p.idesc, (kb != it.kb0 || ks != 0) ? 1u : 0u);
         umma_commit<CG>(c.empty0 + 8u * stage);              // frees the smem slot when MMAs finish
       }
       __syncwarp();
@@ -323,7 +408,6 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int num_tiles = p.m0 * p.n0;
   const int cluster_id = blockIdx.x / CG;
   const int num_clusters = gridDim.x / CG;
   const int rows_cta = p.m2 * 128;
@@ -336,11 +420,13 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     const int bboxes = p.nb / p.b_cw;
     const uint32_t bbox_bytes = (uint32_t)(p.bk * p.swz_b);
     const int a_kstep = p.swz_a / ELEM;
-    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
-      const int tm = tile % p.m0, tn = tile / p.m0;
+    Sched sch(p, cluster_id, num_clusters);
+    Item it;
+    while (sch.next(p, &it)) {
+      const int tm = it.tile % p.m0, tn = it.tile / p.m0;
       const int row = tm * (CG * rows_cta) + (int)rank * rows_cta;
       const int colt = tn * (p.n2 * p.n3) + (int)rank * p.nb;
-      for (int kb = 0; kb < p.k0; ++kb) {
+      for (int kb = it.kb0; kb < it.kb1; ++kb) {
         mbar_wait(empty0 + 8u * stage, phase ^ 1u);
         const uint32_t fb = full0 + 8u * stage;
         if (elect_one()) {
@@ -369,7 +455,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
       // MMA sequence is fully unrolled with loop-invariant descriptor words (issue stays far
       // below the 64-128 cycles one MMA occupies the tensor pipe).
       const int code = (p.bk / UK) * 4 + (p.m2 - 1) * 2 + (p.n2 - 1);
-      MmaCtx c{sbase, full0, empty0, tfull0, tempty0, tmem_base, cluster_id, num_clusters, num_tiles};
+      MmaCtx c{sbase, full0, empty0, tfull0, tempty0, tmem_base, cluster_id, num_clusters};
       switch (code) {
 #define TT_MMA_CASE(KS, M2, N2) \
   case KS * 4 + (M2 - 1) * 2 + (N2 - 1): mma_role<KIND, CG, KS, M2, N2>(p, c); break;
@@ -395,10 +481,18 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     uint32_t aphase = 0;
     int sbuf = 0;
     float v[32];
-    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
-      const int tm = tile % p.m0, tn = tile / p.m0;
+    Sched sch(p, cluster_id, num_clusters);
+    Item it;
+    while (sch.next(p, &it)) {
+      const int tm = it.tile % p.m0, tn = it.tile / p.m0;
+      uint32_t* flag = it.split ? p.flags + (it.tile - p.dp_tiles) * CG + rank : nullptr;
+      const bool add = it.split && it.order > 0;           // lower k-blocks: add onto C
       mbar_wait(tfull0 + 8u * acc, aphase);
       tc_fence_after();
+      if (add) {
+        wait_flag(flag, 4u * (uint32_t)it.order);          // the 4 epilogue warps of each piece above
+        fence_proxy_async_global();
+      }
       const int row_cta = tm * (CG * rows_cta) + (int)rank * rows_cta;
       for (int mi = 0; mi < p.m2; ++mi) {
         const int row0 = row_cta + mi * 128 + q * 32;
@@ -419,7 +513,8 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(&tmC, buf, col0 + c0, row0);
+              if (add) tma_reduce_add_2d(&tmC, buf, col0 + c0, row0);
+              else tma_store_2d(&tmC, buf, col0 + c0, row0);
               bulk_commit();
             }
             sbuf ^= 1;
@@ -428,7 +523,14 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             tmem_ld16(taddr + (uint32_t)c0, v);
             float4* dst = reinterpret_cast<float4*>(C + (int64_t)(row0 + lane) * p.N + col0 + c0);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            for (int j = 0; j < 4; ++j) {
+              float4 o = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+              if (add) {
+                const float4 c = dst[j];
+                o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
+              }
+              dst[j] = o;
+            }
           }
         }
       }
@@ -437,6 +539,18 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
       if (lane == 0) {                                     // TMEM drained: MMA may reuse `acc`
         if (CG == 1 || leader) mbar_arrive(tempty0 + 8u * acc);
         else mbar_arrive_cluster(tempty0 + 8u * acc, 0);
+      }
+      if (it.split) {                                      // publish this piece
+        if (lane == 0) {
+          bulk_wait_all();
+          fence_proxy_async_global();
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
+          const uint32_t old = atom_add_release(flag, 1u);
+          if (it.kb0 == 0 && old == 4u * (uint32_t)it.order + 3u) *flag = 0u;   // last piece: reset
+        }
       }
       if (++acc == p.acc_bufs) { acc = 0; aphase ^= 1u; }
     }
@@ -506,6 +620,96 @@ int num_sms() {
   return n;
 }
 
+// Tail split policy: at most kMaxPieces clusters share one tile, so the
+// descending-k chain of TMA reduce-adds per tile stays short.  TT_TAIL_SPLIT=0 disables it.
+constexpr int kMaxPieces = 4;
+
+bool tail_split_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TT_TAIL_SPLIT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <int KIND, int CG>
+bool set_smem_attr(std::string* err) {
+  static bool done = false;
+  if (!done) {
+    if (!cuda_ok(cudaFuncSetAttribute((const void*)&k_umma<KIND, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kSmemPerCta),
+                 err, "cudaFuncSetAttribute(k_umma)"))
+      return false;
+    done = true;
+  }
+  return true;
+}
+
+template <int KIND, int CG>
+int query_clusters(int smem) {
+  std::string err;
+  if (!set_smem_attr<KIND, CG>(&err)) return 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(num_sms() / CG * CG), 1, 1);
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = CG;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, (const void*)&k_umma<KIND, CG>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+// Co-resident clusters of one CTA (1 CTA per SM: launch bounds, TMEM and smem); without a
+// device (build host) the SM count.
+int max_active_clusters(int kind, int cg, int smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, int>, int> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return num_sms() / cg;
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(dev, kind, cg, smem);
+  auto itc = cache.find(key);
+  if (itc != cache.end()) return itc->second;
+  int n = kind == 0 ? (cg == 1 ? query_clusters<0, 1>(smem) : query_clusters<0, 2>(smem))
+                    : (cg == 1 ? query_clusters<1, 1>(smem) : query_clusters<1, 2>(smem));
+  if (n <= 0) n = num_sms() / cg;
+  n = std::min(n, num_sms() / cg);
+  cache[key] = n;
+  return n;
+}
+
+// Per (device, stream) flag words of the tail split, allocated on first use and left zeroed by
+// every launch (the last piece of each tile resets its word), so CUDA-graph replays and
+// back-to-back launches on one stream need no memset; launches on different streams never share.
+uint32_t* split_flags(cudaStream_t stream, std::string* err) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, uint32_t*> flags;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto& f = flags[{dev, stream}];
+  if (!f) {
+    void* ptr = nullptr;
+    const size_t bytes = sizeof(uint32_t) * 2 * 1024;
+    if (!cuda_ok(cudaMalloc(&ptr, bytes), err, "cudaMalloc(split flags)")) return nullptr;
+    if (!cuda_ok(cudaMemset(ptr, 0, bytes), err, "cudaMemset(split flags)")) return nullptr;
+    f = static_cast<uint32_t*>(ptr);
+  }
+  return f;
+}
+
 struct Plan {
   UmmaArgs a;
   int cg, kind;
@@ -564,10 +768,20 @@ void plan_of(const Space& sp, const State& s, Plan* pl) {
             ((M_inst >> 4) << 24);
   pl->cg = m1;
   pl->kind = kind;
-  const int tiles = a.m0 * a.n0;
-  const int max_clusters = num_sms() / m1;
-  pl->grid = std::min(tiles, max_clusters) * m1;
   pl->smem = a.stages * a.stage_bytes + kEpiBytes + 1024 /*align*/ + 8 * (2 * a.stages + 4) + 16;
+  // persistent grid: as many clusters as can be co-resident (the tail split's cross-cluster
+  // waits rely on it), never more than there are tiles unless the tail is split
+  const int tiles = a.m0 * a.n0;
+  const int P = max_active_clusters(kind, m1, pl->smem);
+  a.dp_tiles = tiles;
+  if (tail_split_enabled() && tiles % P != 0 && a.k0 >= 2) {
+    a.sk_tiles = tiles % P;                              // == tiles when tiles < P
+    a.dp_tiles = tiles - a.sk_tiles;
+    a.sk_workers = std::min(P, a.sk_tiles * kMaxPieces);
+    pl->grid = P * m1;
+  } else {
+    pl->grid = std::min(tiles, P) * m1;
+  }
 }
 
 template <int KIND, int CG>
@@ -575,13 +789,7 @@ tt_status launch_t(const Plan& pl, const CUtensorMap& ma, const CUtensorMap& mb,
                    cudaStream_t stream,
                    std::string* err) {
   auto fn = &k_umma<KIND, CG>;
-  static bool attr = false;
-  if (!attr) {
-    if (!cuda_ok(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemPerCta), err,
-                 "cudaFuncSetAttribute(k_umma)"))
-      return TT_E_CUDA;
-    attr = true;
-  }
+  if (!set_smem_attr<KIND, CG>(err)) return TT_E_CUDA;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)pl.grid, 1, 1);
   cfg.blockDim = dim3(256, 1, 1);
@@ -594,7 +802,12 @@ tt_status launch_t(const Plan& pl, const CUtensorMap& ma, const CUtensorMap& mb,
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  if (!cuda_ok(cudaLaunchKernelEx(&cfg, fn, ma, mb, mc, C, pl.a), err, "k_umma launch")) return TT_E_CUDA;
+  UmmaArgs a = pl.a;
+  if (a.sk_tiles) {
+    a.flags = split_flags(stream, err);
+    if (!a.flags) return TT_E_CUDA;
+  }
+  if (!cuda_ok(cudaLaunchKernelEx(&cfg, fn, ma, mb, mc, C, a), err, "k_umma launch")) return TT_E_CUDA;
   return TT_OK;
 }
 
@@ -618,6 +831,8 @@ tt_status umma_bind(const Space& sp, const State& s, tt_launch_info* info, std::
   info->tmem_cols = pl.a.tmem_cols;
   info->acc_buffers = pl.a.acc_bufs;
   info->idesc = pl.a.idesc;
+  info->split_tiles = pl.a.sk_tiles;
+  info->split_workers = pl.a.sk_workers;
   (void)err;
   return TT_OK;
 }

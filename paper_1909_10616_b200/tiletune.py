@@ -71,7 +71,7 @@ class LaunchInfo(C.Structure):
     _fields_ = [("family", i32), ("grid_x", i64), ("grid_y", i64), ("grid_z", i64), ("block_x", i32),
                 ("cluster_x", i32), ("smem_bytes", i32), ("stages", i32), ("tile_m", i32), ("tile_n", i32),
                 ("tile_k", i32), ("tmem_cols", i32), ("acc_buffers", i32), ("idesc", u32), ("reg_tile_m", i32),
-                ("reg_tile_n", i32)]
+                ("reg_tile_n", i32), ("split_tiles", i32), ("split_workers", i32)]
 
 
 EXPORTS = {

@@ -175,6 +175,42 @@ def test_bf16_4096_sampled():
         assert og.normwise_error(C[ii, jj], og.gemm_f64_entries(A, B, ii, jj)) <= 5e-3
 
 
+@pytest.mark.parametrize("fam,cfg", [
+    (3, ((16, 1, 1, 128), (8, 64), (16, 1, 1, 128))),     # 256 tiles: 108-tile tail over 148 CTAs
+    (3, ((8, 2, 1, 128), (8, 64), (8, 1, 1, 256))),       # 64 pair tiles < 74 pairs: all split
+    (3, ((4, 2, 2, 128), (16, 32), (8, 1, 2, 128))),      # 2 x 2 atoms per CTA
+    (3, ((16, 1, 1, 128), (32, 16), (128, 1, 1, 16))),    # n3 = 16: direct-store epilogue adds
+    (2, ((16, 1, 1, 128), (16, 32), (16, 1, 1, 128))),    # tf32
+    (2, ((8, 2, 1, 128), (64, 8), (16, 1, 1, 128))),
+])
+def test_umma_tail_split(fam, cfg):
+    # DESIGN.md §6 tail split: tiles % co-resident clusters != 0, so the last tiles' k-blocks are
+    # shared by up to 4 clusters (TMA store, then descending-k TMA reduce-adds).  Parity vs the
+    # double oracle, bit-reproducible across launches and streams (the flags reset themselves).
+    M = N = 2048
+    K = 512
+    sp = tt.make_space(M, N, K, family=fam)
+    info = tt.binding(sp, cfg)
+    assert info.split_tiles > 0 and 0 < info.split_workers <= 4 * info.split_tiles
+    bf16 = fam == tt.FAM_BF16_UMMA
+    A, B = host_inputs(M, N, K, bf16=bf16)
+    R = og.gemm_f64(A, B)
+    Ad, Bd = to_dev(A, bf16), to_dev(B, bf16)
+    outs = []
+    s2 = torch.cuda.Stream()
+    for stream in (None, None, s2):
+        C = torch.full((M, N), float("nan"), device=DEV)
+        if stream is None:
+            tt.gemm(Ad, Bd, C, fam, cfg)
+        else:
+            with torch.cuda.stream(stream):
+                tt.gemm(Ad, Bd, C, fam, cfg, stream=stream)
+        torch.cuda.synchronize()
+        outs.append(C.cpu().numpy())
+    assert og.normwise_error(outs[0], R) <= 5e-3
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
 # ------------------------------------------------------------------ evaluator and search
 def test_measure_and_errors():
     ctx = tt.Context(0)
