@@ -18,7 +18,9 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -53,7 +55,12 @@ struct UmmaArgs {
   // first sk_workers clusters; the remaining dp_tiles tiles go round-robin to all clusters.
   int dp_tiles, sk_tiles, sk_workers;
   uint32_t* flags;                  // per split tile and CTA rank: completed-writer count x 4
+  uint64_t* trace;                  // debug (TT_UMMA_TRACE): per cluster x item timestamps, or null
 };
+
+// TT_UMMA_TRACE layout: [cluster][kTraceItems][8] u64 = tile, kb0 | kb1 << 16 | order << 32,
+// t(MMA start), t(MMA last issue), t(epilogue: accumulator ready), t(epilogue: flag ok), t(done), 0
+constexpr int kTraceItems = 16;
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -324,9 +331,14 @@ __device__ __forceinline__ void mma_role(const UmmaArgs& p, const MmaCtx& c) {
   uint32_t aphase = 0;
   Sched sch(p, c.cluster_id, c.num_clusters);
   Item it;
+  int item_no = 0;
   while (sch.next(p, &it)) {
     mbar_wait(c.tempty0 + 8u * acc, aphase ^ 1u);
     tc_fence_after();
+    uint64_t* tr = (p.trace && item_no < kTraceItems) ? p.trace + ((int64_t)c.cluster_id * kTraceItems + item_no) * 8 : nullptr;
+    ++item_no;
+    if (tr && elect_one()) tr[2] = globaltimer();
+    __syncwarp();
     const uint32_t dbase = c.tmem_base + (uint32_t)(acc * p.acc_cols);
     for (int kb = it.kb0; kb < it.kb1; ++kb) {
       mbar_wait(c.full0 + 8u * stage, phase);
@@ -347,7 +359,10 @@ __device__ __forceinline__ void mma_role(const UmmaArgs& p, const MmaCtx& c) {
       __syncwarp();
       if (++stage == p.stages) { stage = 0; phase ^= 1u; }
     }
-    if (elect_one()) umma_commit<CG>(c.tfull0 + 8u * acc);   // accumulator ready for the epilogue
+    if (elect_one()) {
+      umma_commit<CG>(c.tfull0 + 8u * acc);                 // accumulator ready for the epilogue
+      if (tr) tr[3] = globaltimer();
+    }
     __syncwarp();
     if (++acc == p.acc_bufs) { acc = 0; aphase ^= 1u; }
   }
@@ -483,16 +498,26 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     float v[32];
     Sched sch(p, cluster_id, num_clusters);
     Item it;
+    int item_no = 0;
     while (sch.next(p, &it)) {
+      uint64_t* tr = (p.trace && q == 0 && lane == 0 && leader && item_no < kTraceItems)
+                         ? p.trace + ((int64_t)cluster_id * kTraceItems + item_no) * 8 : nullptr;
+      ++item_no;
       const int tm = it.tile % p.m0, tn = it.tile / p.m0;
       uint32_t* flag = it.split ? p.flags + (it.tile - p.dp_tiles) * CG + rank : nullptr;
       const bool add = it.split && it.order > 0;           // lower k-blocks: add onto C
       mbar_wait(tfull0 + 8u * acc, aphase);
       tc_fence_after();
+      if (tr) {
+        tr[0] = (uint64_t)it.tile;
+        tr[1] = (uint64_t)it.kb0 | ((uint64_t)it.kb1 << 16) | ((uint64_t)it.order << 32);
+        tr[4] = globaltimer();
+      }
       if (add) {
         wait_flag(flag, 4u * (uint32_t)it.order);          // the 4 epilogue warps of each piece above
         fence_proxy_async_global();
       }
+      if (tr) tr[5] = globaltimer();
       const int row_cta = tm * (CG * rows_cta) + (int)rank * rows_cta;
       for (int mi = 0; mi < p.m2; ++mi) {
         const int row0 = row_cta + mi * 128 + q * 32;
@@ -551,6 +576,10 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
           const uint32_t old = atom_add_release(flag, 1u);
           if (it.kb0 == 0 && old == 4u * (uint32_t)it.order + 3u) *flag = 0u;   // last piece: reset
         }
+      }
+      if (tr) {
+        bulk_wait_all();
+        tr[6] = globaltimer();
       }
       if (++acc == p.acc_bufs) { acc = 0; aphase ^= 1u; }
     }
@@ -621,15 +650,15 @@ int num_sms() {
 }
 
 // Tail split policy: at most kMaxPieces clusters share one tile, so the
-// descending-k chain of TMA reduce-adds per tile stays short.  TT_TAIL_SPLIT=0 disables it.
+// descending-k chain of TMA reduce-adds per tile stays short.  TT_TAIL_SPLIT = 0 disables it,
+// 2 forces it wherever tiles % clusters != 0 (tests), unset / 1 = the measured policy in plan_of.
+// Read at every plan so a process can A/B both schedules.
 constexpr int kMaxPieces = 4;
 
-bool tail_split_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("TT_TAIL_SPLIT");
-    return !(e && e[0] == '0');
-  }();
-  return on;
+int tail_split_mode() {
+  const char* e = std::getenv("TT_TAIL_SPLIT");
+  if (!e || !e[0]) return 1;
+  return e[0] == '0' ? 0 : (e[0] == '2' ? 2 : 1);
 }
 
 template <int KIND, int CG>
@@ -774,7 +803,18 @@ void plan_of(const Space& sp, const State& s, Plan* pl) {
   const int tiles = a.m0 * a.n0;
   const int P = max_active_clusters(kind, m1, pl->smem);
   a.dp_tiles = tiles;
-  if (tail_split_enabled() && tiles % P != 0 && a.k0 >= 2) {
+  // Split only where it measured a win (profiles/r3_tail_split.md): at least one full
+  // data-parallel wave behind which the pieces' extra epilogues (store, then reduce-add chain)
+  // can hide, a double-buffered accumulator (with one buffer the next item's MMAs wait for the
+  // previous piece's whole epilogue), and an estimated saving of >= 8 us (the idle fraction of
+  // the last wave x one tile's MMA time at ~8192 (bf16) / 4096 (tf32) flop/clk/SM, 1.9 GHz).
+  const int rem = tiles % P;
+  const double tile_us = 2.0 * (128.0 * m1 * a.m2) * (double)(a.n2 * a.n3) * (double)a.K /
+                         ((kind == 0 ? 8192.0 : 4096.0) * m1 * 1.9e3);
+  const double gain_us = (1.0 - (double)rem / P) * tile_us;
+  const int mode = tail_split_mode();
+  const bool worth = tiles - rem >= P && a.acc_bufs == 2 && gain_us >= 8.0;
+  if (mode != 0 && rem != 0 && a.k0 >= 2 && (mode == 2 || worth)) {
     a.sk_tiles = tiles % P;                              // == tiles when tiles < P
     a.dp_tiles = tiles - a.sk_tiles;
     a.sk_workers = std::min(P, a.sk_tiles * kMaxPieces);
@@ -807,7 +847,25 @@ tt_status launch_t(const Plan& pl, const CUtensorMap& ma, const CUtensorMap& mb,
     a.flags = split_flags(stream, err);
     if (!a.flags) return TT_E_CUDA;
   }
+  static const char* trace_path = std::getenv("TT_UMMA_TRACE");
+  const size_t trace_words = (size_t)(pl.grid / CG) * kTraceItems * 8;
+  if (trace_path) {
+    if (!cuda_ok(cudaMalloc(&a.trace, trace_words * 8), err, "cudaMalloc(trace)")) return TT_E_CUDA;
+    cudaMemsetAsync(a.trace, 0, trace_words * 8, stream);
+  }
   if (!cuda_ok(cudaLaunchKernelEx(&cfg, fn, ma, mb, mc, C, a), err, "k_umma launch")) return TT_E_CUDA;
+  if (trace_path) {                                         // debug only: synchronous dump
+    std::vector<uint64_t> h(trace_words);
+    if (!cuda_ok(cudaStreamSynchronize(stream), err, "trace sync")) return TT_E_CUDA;
+    cudaMemcpy(h.data(), a.trace, trace_words * 8, cudaMemcpyDeviceToHost);
+    cudaFree(a.trace);
+    if (FILE* f = std::fopen(trace_path, "ab")) {
+      const uint64_t hdr[4] = {(uint64_t)(pl.grid / CG), (uint64_t)kTraceItems, (uint64_t)a.dp_tiles, (uint64_t)a.sk_tiles};
+      std::fwrite(hdr, 8, 4, f);
+      std::fwrite(h.data(), 8, h.size(), f);
+      std::fclose(f);
+    }
+  }
   return TT_OK;
 }
 

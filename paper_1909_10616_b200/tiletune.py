@@ -230,6 +230,8 @@ def _stream(stream) -> Optional[int]:
     if stream is None:
         import torch
         return torch.cuda.current_stream().cuda_stream
+    if hasattr(stream, "cuda_stream"):                   # torch.cuda.Stream
+        return stream.cuda_stream
     return int(stream)
 
 

@@ -268,3 +268,19 @@ def test_na2c_T_decay_schedule_parity():
     # the schedule changes the traversal relative to a constant T = 8
     const = tt.na2c_search(64, 64, 64, 250, tt.search_opts(seed=2, epsilon=0.0, steps_T=8, batch=6), table=tab)
     assert _trace_key(const.trace) != _trace_key(lres.trace)
+
+
+def test_umma_tail_split_policy(monkeypatch):
+    # default policy (runs with and without a GPU: 74 co-resident pairs either way): split 4096^3 bf16 256-pair-tile configs (one full wave of
+    # data-parallel tiles, double-buffered accumulator, >= 8 us estimated saving); never when
+    # every tile would be split or the accumulator is single-buffered; TT_TAIL_SPLIT=0 disables
+    monkeypatch.delenv("TT_TAIL_SPLIT", raising=False)
+    sp = tt.make_space(4096, 4096, 4096, family=3)
+    assert tt.binding(sp, ((16, 2, 1, 128), (32, 128), (16, 1, 1, 256))).split_tiles == 256 % 74
+    assert tt.binding(sp, ((16, 2, 1, 128), (64, 64), (8, 1, 2, 256))).split_tiles == 0       # 512 acc columns
+    assert tt.binding(tt.make_space(1024, 8192, 8192, family=3),
+                      ((2, 2, 2, 128), (128, 64), (32, 1, 1, 256))).split_tiles == 0          # 64 tiles < 74
+    assert tt.binding(tt.make_space(2048, 2048, 2048, family=3),
+                      ((16, 1, 1, 128), (16, 128), (16, 1, 1, 128))).split_tiles == 0        # saving < 8 us
+    monkeypatch.setenv("TT_TAIL_SPLIT", "0")
+    assert tt.binding(sp, ((16, 2, 1, 128), (32, 128), (16, 1, 1, 256))).split_tiles == 0

@@ -36,7 +36,8 @@ order = sorted(range(len(cfgs)), key=lambda i: costs[i])
 best = costs[order[0]]
 res = {"problem": [a.m, a.k, a.n], "family": a.family, "feasible": len(cfgs), "sweep_s": sweep_s,
        "exhaustive_best_s": best, "exhaustive_best": cli.encode(cfgs[order[0]]),
-       "top10": [(cli.encode(cfgs[i]), costs[i]) for i in order[:10]], "gbfs": []}
+       "top10": [(cli.encode(cfgs[i]), costs[i]) for i in order[:10]], "gbfs": [],
+       "all": [(cli.encode(c), x) for c, x in zip(cfgs, costs)]}
 flops = 2.0 * a.m * a.n * a.k
 for seed in cli.parse_seeds(a.seeds):
     r = tt.gbfs_search(a.m, a.n, a.k, a.budget, tt.search_opts(family=fam, seed=seed, measure={"repeats": a.repeats}),
@@ -47,4 +48,4 @@ for seed in cli.parse_seeds(a.seeds):
 res["exhaustive_best_tflops"] = flops / best / 1e12
 with open(a.out + ".json", "w") as f:
     json.dump(res, f, indent=1)
-print(json.dumps({k: v for k, v in res.items() if k not in ("top10", "gbfs")}))
+print(json.dumps({k: v for k, v in res.items() if k not in ("top10", "gbfs", "all")}))

@@ -1,0 +1,73 @@
+"""Debug timeline of the persistent tcgen05 kernel (TT_UMMA_TRACE, DESIGN.md §6 tail split).
+
+Runs one config a few times with the item trace on and prints, per cluster, each item's tile,
+k-range, order and timestamps relative to the kernel's earliest MMA start (us)."""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--m", type=int, default=4096)
+    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--k", type=int, default=4096)
+    ap.add_argument("--family", default="bf16")
+    ap.add_argument("--config", required=True)
+    ap.add_argument("--out", default="gpurun_out/umma_trace.bin")
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    if os.path.exists(a.out):
+        os.remove(a.out)
+    os.environ["TT_UMMA_TRACE"] = a.out
+    import torch
+    from paper_1909_10616_b200 import tiletune as tt
+    fam = {"bf16": tt.FAM_BF16_UMMA, "tf32": tt.FAM_TF32_UMMA}[a.family]
+    cfg = json.loads(a.config)
+    s = (tuple(cfg["m"]), tuple(cfg["k"]), tuple(cfg["n"]))
+    dt = torch.bfloat16 if a.family == "bf16" else torch.float32
+    A = torch.randn(a.m, a.k, device="cuda").to(dt)
+    B = torch.randn(a.k, a.n, device="cuda").to(dt)
+    C = torch.empty(a.m, a.n, device="cuda")
+    for _ in range(a.reps):
+        tt.gemm(A, B, C, fam, s)
+    torch.cuda.synchronize()
+    raw = np.fromfile(a.out, dtype=np.uint64)
+    pos = 0
+    rep = 0
+    while pos < raw.size:
+        ncl, nit, dp, sk = (int(x) for x in raw[pos:pos + 4])
+        pos += 4
+        tr = raw[pos:pos + ncl * nit * 8].reshape(ncl, nit, 8).astype(np.int64)
+        pos += ncl * nit * 8
+        rep += 1
+        if rep < a.reps:
+            continue
+        valid = tr[:, :, 2] > 0
+        t0 = tr[:, :, 2][valid].min()
+        end = tr[:, :, 6][valid].max()
+        print(f"clusters {ncl} dp_tiles {dp} sk_tiles {sk} kernel span {(end - t0) / 1e3:.2f} us")
+        ends = []
+        for c in range(ncl):
+            items = []
+            for i in range(nit):
+                if tr[c, i, 2] == 0:
+                    break
+                tile, w, ms, me, ea, ef, ed, _ = tr[c, i]
+                kb0, kb1, order = w & 0xFFFF, (w >> 16) & 0xFFFF, w >> 32
+                items.append(f"t{tile}[{kb0},{kb1})o{order} mma {(ms - t0) / 1e3:.1f}-{(me - t0) / 1e3:.1f} "
+                             f"epi {(ea - t0) / 1e3:.1f}/{(ef - t0) / 1e3:.1f}/{(ed - t0) / 1e3:.1f}")
+            ends.append((tr[c, :, 6].max() - t0) / 1e3)
+            if c < 12 or c % 10 == 0:
+                print(f"c{c:3d}: " + " | ".join(items))
+        ends = np.array(ends)
+        print(f"cluster end us: min {ends.min():.1f} median {np.median(ends):.1f} max {ends.max():.1f}")
+
+
+if __name__ == "__main__":
+    main()
