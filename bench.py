@@ -43,8 +43,9 @@ WORKLOADS = {
     "bf16_8192": (8192, 8192, 8192, 3, 64),
     "tf32_2048": (2048, 2048, 2048, 2, 64),
     "tf32_4096": (4096, 4096, 4096, 2, 64),
-    "f32_4096": (4096, 4096, 4096, 1, 256),
-    "f32_2048": (2048, 2048, 2048, 1, 256),
+    # fp32 SIMT: 0.1 % of the raw space (the paper's budget, P:375 / P:397), s0 untiled
+    "f32_4096": (4096, 4096, 4096, 1, 2691),
+    "f32_2048": (2048, 2048, 2048, 1, 1590),
     "f32_512": (512, 512, 512, 1, 484),
 }
 FAMILY_DTYPE = {1: "f32", 2: "tf32", 3: "bf16"}

@@ -136,6 +136,29 @@ def _run(strategy, args, seed, ctx):
         opts.s0 = tt.to_config(decode(args.start_config, (args.dm, args.dk, args.dn)))
     fn = {"gbfs": tt.gbfs_search, "na2c": tt.na2c_search, "random": tt.random_search}[strategy]
     recorded = _load_resume(args, strategy, seed)
+    if recorded is None and getattr(args, "shared_cache", False) and args.backend == "device":
+        # One measurement per distinct state for the whole compare run: every search that reaches
+        # a state gets the cost measured the first time (the same hardware test, so strategies are
+        # compared on common measurements).  `equiv_wall` = what this search's own measurements
+        # took when they were first made, i.e. its stand-alone tuning wall-time.
+        sp = _space(args)
+        mo = tt.measure_opts(repeats=args.repeats, warmup=args.warmup)
+        cache = args._cost_cache
+        equiv = [0.0]
+
+        def cached(states):
+            out = []
+            for s in states:
+                if s not in cache:
+                    t0 = time.perf_counter()
+                    c = ctx.measure(sp, s, mo).cost_s
+                    cache[s] = (c, time.perf_counter() - t0)
+                out.append(cache[s][0])
+                equiv[0] += cache[s][1]
+            return out
+        res = fn(args.m, args.n, args.k, args.max_evals, opts, batch=cached)
+        res.equiv_wall_s = equiv[0]
+        return res
     if recorded is None:
         kw = {"ctx": ctx} if args.backend == "device" else {"cost": synthetic_cost(args)}
         return fn(args.m, args.n, args.k, args.max_evals, opts, **kw)
@@ -177,18 +200,24 @@ def _tune(args, strategies):
                                      "family": args.family, "backend": args.backend},
                          "seeds": seeds, "max_evals": args.max_evals, "strategies": {}}
     flops = 2.0 * args.m * args.n * args.k
+    args._cost_cache = {}
     for strat in strategies:
-        bests, walls = [], []
+        bests, walls, equivs = [], [], []
         for seed in seeds:
             res = _run(strat, args, seed, ctx)
             bests.append(res.best_cost)
             walls.append(res.wall_s)
+            if hasattr(res, "equiv_wall_s"):
+                equivs.append(res.equiv_wall_s)
             for r in res.trace:
                 rows.append([strat, seed, r["eval_index"], f"{r['t_wall_s']:.6f}", encode(r["state"]), repr(r["cost"]),
                              repr(r["best"]), f"{(r['eval_index'] + 1) / res.space_raw:.9f}"])
             print(f"{strat} seed {seed}: best {res.best_cost:.6g} after {res.evals} evals "
                   f"({100 * res.frac_raw:.4f}% of {res.space_raw}, {res.wall_s:.1f} s) {encode(res.best)}", flush=True)
         st = {"best_cost": box(bests), "wall_s": box(walls)}
+        if equivs:
+            st["equiv_wall_s"] = box(equivs)
+            summary["distinct_states_measured"] = len(args._cost_cache)
         if args.backend == "device":
             st["best_tflops"] = box([flops / c / 1e12 for c in bests])
         summary["strategies"][strat] = st
@@ -271,6 +300,8 @@ def main(argv=None):
         p.add_argument("--start-config", default=None)
         p.add_argument("--out", default="runs/tune")
         p.add_argument("--resume", default=None, help="CSV trace of an earlier run: replay it, then continue")
+        p.add_argument("--shared-cache", action="store_true",
+                       help="device: measure each distinct state once for the whole run (common measurements)")
         p.set_defaults(fn=fn)
     args = ap.parse_args(argv)
     args.fn(args)
