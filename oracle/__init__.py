@@ -24,6 +24,7 @@ Modules
   gemm     -- C = A.B in double and in sequential-k fp32 fmaf (P:113, P:125,
               P:166); the arithmetic lives in gemm_ref.c
 
-Parity status: every function is pinned by ``tests/test_oracle_*.py`` except
-the exact N-A2C trajectory with epsilon > 0 ("parity unpinned").
+Parity status: every function is pinned by ``tests/test_oracle_*.py``.  The
+N-A2C networks sum in a fixed order with C-library transcendentals (reading
+Z24), so library trajectories are compared exactly at every eps.
 """

@@ -37,8 +37,10 @@ a guided by the policy").  Readings (Z18):
   * policy sampling: u = uniform(); first legitimate action (action order) whose cumulative
     probability exceeds u, else the last legitimate one.
 With eps = 0 the policy is never consulted, so the trajectory depends only on the RNG and the
-cost source: that mode is bit-exact against the library.  With eps > 0 exact trajectories
-depend on floating-point summation order: parity unpinned (properties only).
+cost source.  With eps > 0 the trajectory also depends on the networks; their arithmetic is
+written with every sum left-to-right in index order and C-library tanh / exp / log (mlp.py,
+reading Z24), so the whole trajectory is still a fixed function of (seed, costs) and the
+library is compared bit for bit in both modes.
 """
 from __future__ import annotations
 
@@ -78,10 +80,15 @@ class Agent:
         self.critic = Mlp([nin, p.hidden, p.hidden, 1], rng_nn)
 
     def legal_mask(self, s) -> np.ndarray:
+        """Which actions lead to a legitimate state (a pure function of s, memoised)."""
+        cache = self.__dict__.setdefault("_mask_cache", {})
+        if s in cache:
+            return cache[s]
         m = np.zeros(len(self.acts), dtype=bool)
         for i, a in enumerate(self.acts):
             t = space.step(s, a)
             m[i] = t is not None and space.legitimate(self.spec, t)
+        cache[s] = m
         return m
 
     def policy(self, s) -> np.ndarray:
@@ -112,12 +119,19 @@ class Agent:
             dz = np.zeros_like(z)
             for b in range(B):
                 pi = masked_softmax(z[b], masks[b])
-                logpi = np.where(masks[b], np.log(np.where(masks[b], pi, 1.0)), 0.0)
-                H = -float((pi * logpi).sum())
-                g = -adv[b] * (-pi)
-                g[aidx[b]] += -adv[b]
-                g += p.beta * pi * (logpi + H)
-                dz[b] = np.where(masks[b], g, 0.0) / B
+                H = 0.0                                             # entropy, left-to-right
+                for i in range(len(pi)):
+                    if masks[b][i] and pi[i] > 0:
+                        H -= pi[i] * math.log(pi[i])
+                for i in range(len(pi)):
+                    if not masks[b][i]:
+                        continue
+                    lp = math.log(pi[i]) if pi[i] > 0 else 0.0
+                    g = adv[b] * pi[i]                              # d(-A log pi_a)/dz_i = A (pi_i - [i = a])
+                    if i == aidx[b]:
+                        g -= adv[b]
+                    g += p.beta * pi[i] * (lp + H)                  # d(-beta H)/dz_i
+                    dz[b, i] = g / B
             gWa, gba = self.actor.backward(acts_a, dz)
             self.critic.sgd_step(gWc, gbc, p.lr, p.clip)
             self.actor.sgd_step(gWa, gba, p.lr, p.clip)

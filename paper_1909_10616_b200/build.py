@@ -42,6 +42,8 @@ def _compile(src: str) -> str:
            "-Xcompiler", "-fPIC", "-I", INCLUDE] + ARCH
     if src.endswith(".cu"):
         cmd += ["-Xptxas", "-v"] if os.environ.get("TT_PTXAS_VERBOSE") else []
+    else:   # host search code: no mul-add contraction, so the N-A2C MLP sums exactly as written (Z24)
+        cmd += ["-Xcompiler", "-ffp-contract=off"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")

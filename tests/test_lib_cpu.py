@@ -206,8 +206,30 @@ def test_na2c_eps0_small_batch_parity():
     assert _trace_key(lres.trace) == _oracle_key(o)
 
 
+@pytest.mark.parametrize("seed,table,budget,kw", [
+    (0, "t2", 200, {}),
+    (1, "t1", 200, {}),
+    (2, "t2", 160, {"batch": 8, "steps": 2, "gamma": 0.5}),
+])
+def test_na2c_policy_trace_parity(seed, table, budget, kw):
+    # epsilon = 0.8 (the policy is followed with probability eps): the actor is sampled
+    # and both networks are trained after every batch, so the traversal depends on the MLP
+    # arithmetic.  Oracle and library sum in the same order with the same libm (reading Z24):
+    # the traces, i.e. every state and cost in order, must be identical.
+    sp = Spec(64, 64, 64)
+    f = (lambda s: costs.t2_cost(sp, s)) if table == "t2" else costs.t1_cost
+    tab = costs.table(sp, f)
+    p = ona2c.Params(epsilon=0.8, **kw)
+    o = ona2c.na2c(sp, ogbfs.table_source(sp, tab), budget=budget, params=p, seed=seed)
+    lo = {"batch": "batch", "steps": "steps_T", "gamma": "gamma"}
+    lres = tt.na2c_search(64, 64, 64, budget, tt.search_opts(seed=seed, epsilon=0.8, **{lo[k]: v for k, v in kw.items()}),
+                          table=tab)
+    assert _trace_key(lres.trace) == _oracle_key(o)
+    assert lres.best_cost == o.best_cost
+
+
 def test_na2c_policy_properties():
-    # epsilon = 0.8 (policy consulted): exact trajectory is parity-unpinned; check the invariants
+    # epsilon = 0.8 (policy consulted): invariants and search quality on top of the trace parity
     sp = Spec(64, 64, 64)
     res = tt.na2c_search(64, 64, 64, 988, tt.search_opts(seed=3), cost=costs.t1_cost)
     states = [r["state"] for r in res.trace]
