@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define TT_VERSION 3
+#define TT_VERSION 4
 #define TT_MAXD 4  /* maximum loop depth per axis carried in tt_config */
 
 typedef enum {
@@ -79,6 +79,8 @@ typedef struct {
   int32_t number;          /* back-to-back launches per repeat */
   int32_t device;          /* CUDA ordinal the sample was taken on */
   int32_t slow_cut;        /* 1 if cost_s = probe_s because probe_s > cut_s (Z12) */
+  int32_t graph_nodes;     /* launches per captured CUDA graph the repeats replayed (0: direct launches) */
+  int32_t reserved;
 } tt_sample;
 
 typedef struct {
@@ -88,6 +90,9 @@ typedef struct {
   double cut_s;            /* if > 0 and probe > cut_s: cost = probe, repeats = 1 (Z12) */
   int32_t l2_flush;        /* 1: overwrite a >= 2 x L2 buffer before every timed launch */
   int32_t max_number;      /* cap on `number` (default 1000) */
+  int32_t graph;           /* 1 (default): each repeat replays a CUDA graph of up to 32 captured
+                              launches, so host launch overhead never enters the score; 0: direct
+                              launches from the host loop.  Ignored with l2_flush. */
 } tt_measure_opts;
 
 /* One row per measured state, in evaluation order (Fig. 7 axes P:352). */
@@ -262,7 +267,8 @@ tt_status tt_ctx_operands(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, int32_t 
 /* cost(s) on hardware ("test (i.e., run the configuration on target hardware)"):
  * one cold timed probe (if it exceeds opts->cut_s the candidate is scored by it, Z12), warmup
  * launches, a warm probe that sizes `number`, then R repeats of `number` launches between CUDA
- * events on the ctx stream; cost = median of per-repeat means (Z10).  The measured operands are
+ * events on the ctx stream (replayed from a captured CUDA graph unless opts->graph = 0, so the
+ * score is device time, not host launch rate); cost = median of per-repeat means (Z10).  The measured operands are
  * the ctx's (K4 recipe); the space's layout selects the NN or TN kernel.  TT_E_ILLEGITIMATE / TT_E_INFEASIBLE for a config
  * without J; TT_E_CUDA on a launch error. */
 tt_status tt_measure(tt_ctx* ctx, const tt_space* sp, const tt_config* cfg,

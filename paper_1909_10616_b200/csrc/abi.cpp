@@ -149,6 +149,7 @@ void tt_measure_opts_default(tt_measure_opts* m) {
   m->cut_s = 0.0;
   m->l2_flush = 0;
   m->max_number = 1000;
+  m->graph = 1;
 }
 
 void tt_search_opts_default(tt_search_opts* o) {

@@ -182,20 +182,60 @@ tt_status Ctx::measure(const Space& sp, const State& s, const tt_measure_opts& m
   out->probe_s = probe;
   float ms = 0;
   const int R = std::max(1, std::min(mo.repeats > 0 ? mo.repeats : 10, kMaxRepeats));
+  const double mr = mo.min_repeat_s > 0 ? mo.min_repeat_s : 5e-4;
+  const int max_number = mo.max_number > 0 ? mo.max_number : 1000;
   int number = 1;
   if (!mo.l2_flush) {
-    const double mr = mo.min_repeat_s > 0 ? mo.min_repeat_s : 5e-4;
     number = (int)std::ceil(mr / std::max(probe, 1e-9));
-    number = std::max(1, std::min(number, mo.max_number > 0 ? mo.max_number : 1000));
+    number = std::max(1, std::min(number, max_number));
+  }
+  // Graph mode: capture up to kGraphNodes launches once and replay the graph, so a repeat is
+  // pure device time even when the kernel is shorter than the host's launch path (tensor-map
+  // encoding, cluster launch).  `number` is re-sized from one timed graph replay.
+  cudaGraphExec_t ge = nullptr;
+  int nodes = 0, glaunch = 0;
+  if (mo.graph != 0 && !mo.l2_flush) {
+    nodes = std::min(number, kGraphNodes);
+    cudaGraph_t g = nullptr;
+    tt_status ls = TT_OK;
+    if (cudaStreamBeginCapture(stream, cudaStreamCaptureModeRelaxed) == cudaSuccess) {
+      for (int i = 0; i < nodes && ls == TT_OK; ++i) ls = launch();
+      const cudaError_t ce = cudaStreamEndCapture(stream, &g);
+      if (ls != TT_OK || ce != cudaSuccess || cudaGraphInstantiate(&ge, g, 0) != cudaSuccess) ge = nullptr;
+      if (g) cudaGraphDestroy(g);
+    }
+    cudaGetLastError();                                  // a failed capture leaves direct launches
+    if (ge) {
+      cudaGraphLaunch(ge, stream);                       // untimed: uploads the graph
+      cudaEventRecord(ev[0], stream);
+      cudaGraphLaunch(ge, stream);
+      cudaEventRecord(ev[1], stream);
+      if (!cuda_ok(cudaEventSynchronize(ev[1]), err, "graph probe")) {
+        cudaGraphExecDestroy(ge);
+        return TT_E_CUDA;
+      }
+      cudaEventElapsedTime(&ms, ev[0], ev[1]);
+      const double per_graph = std::max(ms * 1e-3, 1e-9);
+      glaunch = std::max(1, std::min((int)std::ceil(mr / per_graph), std::max(1, max_number / nodes)));
+      number = nodes * glaunch;
+    } else {
+      nodes = 0;
+    }
   }
   for (int r = 0; r < R; ++r) {
     if (mo.l2_flush && (st = flush_l2(err)) != TT_OK) return st;
     cudaEventRecord(ev[2 + 2 * r], stream);
-    for (int i = 0; i < number; ++i)
-      if ((st = launch()) != TT_OK) return st;
+    if (ge) {
+      for (int j = 0; j < glaunch; ++j) cudaGraphLaunch(ge, stream);
+    } else {
+      for (int i = 0; i < number; ++i)
+        if ((st = launch()) != TT_OK) return st;
+    }
     cudaEventRecord(ev[3 + 2 * r], stream);
   }
-  if (!cuda_ok(cudaEventSynchronize(ev[1 + 2 * R]), err, "measure")) return TT_E_CUDA;
+  const bool synced = cuda_ok(cudaEventSynchronize(ev[1 + 2 * R]), err, "measure");
+  if (ge) cudaGraphExecDestroy(ge);
+  if (!synced) return TT_E_CUDA;
   std::vector<double> per(R);
   for (int r = 0; r < R; ++r) {
     cudaEventElapsedTime(&ms, ev[2 + 2 * r], ev[3 + 2 * r]);
@@ -214,6 +254,7 @@ tt_status Ctx::measure(const Space& sp, const State& s, const tt_measure_opts& m
   out->stdev_s = R > 1 ? std::sqrt(var / (R - 1)) : 0.0;
   out->repeats = R;
   out->number = number;
+  out->graph_nodes = nodes;
   return cuda_ok(cudaGetLastError(), err, "measure") ? TT_OK : TT_E_CUDA;
 }
 

@@ -13,6 +13,7 @@ struct tt_ctx {};  // opaque ABI handle; tt::Ctx derives from it
 namespace tt {
 
 constexpr int kMaxRepeats = 64;
+constexpr int kGraphNodes = 32;   // launches captured per measurement graph
 
 struct Operands {
   int64_t M = 0, N = 0, K = 0;

@@ -895,9 +895,29 @@ tt_status umma_bind(const Space& sp, const State& s, tt_launch_info* info, std::
   return TT_OK;
 }
 
-tt_status umma_launch(const Space& sp, const State& s, const void* A, const void* B, float* C, cudaStream_t stream,
-                      std::string* err) {
+namespace {
+
+// Host launch path cache: plan + three tensor maps per (device, problem, config, pointers,
+// tail-split mode).  Encoding three tensor maps costs microseconds of host time per launch,
+// as long as a small GEMM runs on the device; repeated launches of one config (the evaluator,
+// a training loop) reuse them.  Bounded: cleared when it reaches kLaunchCacheMax entries.
+struct LaunchKey {
+  int dev, family, layout, split_mode;
+  int64_t dims[3];
+  int64_t f[3][TT_MAXD];
+  const void *A, *B;
+  float* C;
+  bool operator<(const LaunchKey& o) const { return std::memcmp(this, &o, sizeof(LaunchKey)) < 0; }
+};
+struct LaunchEntry {
   Plan pl;
+  CUtensorMap ma, mb, mc;
+};
+constexpr size_t kLaunchCacheMax = 512;
+
+tt_status prepare(const Space& sp, const State& s, const void* A, const void* B, float* C, LaunchEntry* e,
+                  std::string* err) {
+  Plan& pl = e->pl;
   plan_of(sp, s, &pl);
   if (((uintptr_t)A % 16) || ((uintptr_t)B % 16) || ((uintptr_t)C % 16)) {
     *err = "UMMA family needs 16-byte aligned A, B, C";
@@ -908,23 +928,65 @@ tt_status umma_launch(const Space& sp, const State& s, const void* A, const void
     *err = "UMMA family needs row pitches that are multiples of 16 bytes";
     return TT_E_UNSUPPORTED;
   }
-  CUtensorMap ma, mb, mc;
   if (pl.a.a_mn) {
-    if (!make_map(&ma, pl.kind, A, (uint64_t)pl.a.M, (uint64_t)pl.a.K, (uint32_t)pl.a.a_cw, (uint32_t)pl.a.bk,
+    if (!make_map(&e->ma, pl.kind, A, (uint64_t)pl.a.M, (uint64_t)pl.a.K, (uint32_t)pl.a.a_cw, (uint32_t)pl.a.bk,
                   pl.kind == 1 ? -128 : 128, err))
       return TT_E_CUDA;
-  } else if (!make_map(&ma, pl.kind, A, (uint64_t)pl.a.K, (uint64_t)pl.a.M, (uint32_t)(pl.a.swz_a / elem),
-                (uint32_t)(pl.a.m2 * 128), pl.a.swz_a, err))
+  } else if (!make_map(&e->ma, pl.kind, A, (uint64_t)pl.a.K, (uint64_t)pl.a.M, (uint32_t)(pl.a.swz_a / elem),
+                       (uint32_t)(pl.a.m2 * 128), pl.a.swz_a, err)) {
     return TT_E_CUDA;
-  if (!make_map(&mb, pl.kind, B, (uint64_t)pl.a.N, (uint64_t)pl.a.K, (uint32_t)pl.a.b_cw, (uint32_t)pl.a.bk,
+  }
+  if (!make_map(&e->mb, pl.kind, B, (uint64_t)pl.a.N, (uint64_t)pl.a.K, (uint32_t)pl.a.b_cw, (uint32_t)pl.a.bk,
                 pl.a.b_layout == 1 ? -128 : pl.a.swz_b, err))
     return TT_E_CUDA;
   // C: fp32 [M][N], 32 x 32 boxes, 128B swizzle (matches the epilogue staging layout)
-  if (!make_map(&mc, 1, C, (uint64_t)pl.a.N, (uint64_t)pl.a.M, 32u, 32u, 128, err)) return TT_E_CUDA;
-  if (pl.kind == 0) {
-    return pl.cg == 1 ? launch_t<0, 1>(pl, ma, mb, mc, C, stream, err) : launch_t<0, 2>(pl, ma, mb, mc, C, stream, err);
+  if (!make_map(&e->mc, 1, C, (uint64_t)pl.a.N, (uint64_t)pl.a.M, 32u, 32u, 128, err)) return TT_E_CUDA;
+  return TT_OK;
+}
+
+}  // namespace
+
+tt_status umma_launch(const Space& sp, const State& s, const void* A, const void* B, float* C, cudaStream_t stream,
+                      std::string* err) {
+  static std::mutex mu;
+  static std::map<LaunchKey, LaunchEntry> cache;
+  LaunchKey k;
+  std::memset(&k, 0, sizeof(k));                          // padding bytes take part in the compare
+  cudaGetDevice(&k.dev);
+  k.family = sp.family;
+  k.layout = sp.layout;
+  k.split_mode = tail_split_mode();
+  for (int a = 0; a < 3; ++a) {
+    k.dims[a] = sp.dim[a];
+    for (int i = 0; i < TT_MAXD; ++i) k.f[a][i] = s.f[a][i];
   }
-  return pl.cg == 1 ? launch_t<1, 1>(pl, ma, mb, mc, C, stream, err) : launch_t<1, 2>(pl, ma, mb, mc, C, stream, err);
+  k.A = A;
+  k.B = B;
+  k.C = C;
+  LaunchEntry e;
+  bool hit = false;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(k);
+    if (it != cache.end()) {
+      e = it->second;
+      hit = true;
+    }
+  }
+  if (!hit) {
+    tt_status st = prepare(sp, s, A, B, C, &e, err);
+    if (st != TT_OK) return st;
+    std::lock_guard<std::mutex> lk(mu);
+    if (cache.size() >= kLaunchCacheMax) cache.clear();
+    cache.emplace(k, e);
+  }
+  const Plan& pl = e.pl;
+  if (pl.kind == 0) {
+    return pl.cg == 1 ? launch_t<0, 1>(pl, e.ma, e.mb, e.mc, C, stream, err)
+                      : launch_t<0, 2>(pl, e.ma, e.mb, e.mc, C, stream, err);
+  }
+  return pl.cg == 1 ? launch_t<1, 1>(pl, e.ma, e.mb, e.mc, C, stream, err)
+                    : launch_t<1, 2>(pl, e.ma, e.mb, e.mc, C, stream, err);
 }
 
 }  // namespace tt

@@ -35,12 +35,13 @@ class Config(C.Structure):
 
 class Sample(C.Structure):
     _fields_ = [("cost_s", dbl), ("mean_s", dbl), ("min_s", dbl), ("stdev_s", dbl), ("probe_s", dbl),
-                ("repeats", i32), ("number", i32), ("device", i32), ("slow_cut", i32)]
+                ("repeats", i32), ("number", i32), ("device", i32), ("slow_cut", i32), ("graph_nodes", i32),
+                ("reserved", i32)]
 
 
 class MeasureOpts(C.Structure):
     _fields_ = [("warmup", i32), ("repeats", i32), ("min_repeat_s", dbl), ("cut_s", dbl), ("l2_flush", i32),
-                ("max_number", i32)]
+                ("max_number", i32), ("graph", i32)]
 
 
 class TraceRow(C.Structure):

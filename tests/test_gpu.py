@@ -230,7 +230,25 @@ def test_measure_and_errors():
     cut = ctx.measure(sp, space.initial_state(Spec(512, 512, 512)), tt.measure_opts(cut_s=1e-6))
     assert cut.slow_cut == 1 and cut.repeats == 1
     fl = ctx.measure(sp, ((4, 2, 8, 8), (64, 8), (4, 4, 4, 8)), tt.measure_opts(l2_flush=1, repeats=3))
-    assert fl.number == 1 and fl.repeats == 3
+    assert fl.number == 1 and fl.repeats == 3 and fl.graph_nodes == 0
+
+
+def test_measure_graph_replay():
+    # default: repeats replay a captured CUDA graph (device time only); graph=0: host launch loop.
+    # On a ~5 us bf16 GEMM the host path (tensor maps, cluster launch) can exceed the kernel, so
+    # the graph score must not be slower, and both must agree on a long kernel.
+    ctx = tt.Context(0)
+    small = tt.make_space(1024, 1024, 1024, family=3)
+    cfg = ((8, 1, 1, 128), (8, 128), (16, 1, 1, 64))
+    g = ctx.measure(small, cfg)
+    d = ctx.measure(small, cfg, tt.measure_opts(graph=0))
+    assert g.graph_nodes > 0 and d.graph_nodes == 0 and g.number % g.graph_nodes == 0
+    assert g.cost_s <= d.cost_s * 1.05, (g.cost_s, d.cost_s)
+    big = tt.make_space(4096, 4096, 4096, family=3)
+    cfg = ((16, 2, 1, 128), (32, 128), (16, 1, 1, 256))
+    g = ctx.measure(big, cfg, tt.measure_opts(repeats=5))
+    d = ctx.measure(big, cfg, tt.measure_opts(repeats=5, graph=0))
+    assert abs(g.cost_s / d.cost_s - 1) < 0.05, (g.cost_s, d.cost_s)
     ctx.close()
 
 
