@@ -47,6 +47,9 @@ WORKLOADS = {
     "f32_4096": (4096, 4096, 4096, 1, 2691),
     "f32_2048": (2048, 2048, 2048, 1, 1590),
     "f32_512": (512, 512, 512, 1, 484),
+    # the paper's main experiment shape: 0.1 % of 899 756 states
+    "f32_1024": (1024, 1024, 1024, 1, 900),
+    "bf16_1024": (1024, 1024, 1024, 3, 64),
 }
 FAMILY_DTYPE = {1: "f32", 2: "tf32", 3: "bf16"}
 
@@ -389,6 +392,13 @@ def main():
         peak_note = f"fp32 FFMA: 148 SM x 128 lanes x 2 x {smx:.0f} MHz (DESIGN.md §6)"
         bound = "alu"
     achieved = flops_rank / (ms_local * 1e-3) / 1e12
+    # memory side of the same launch: compulsory bytes (A, B in at the input width, C out fp32)
+    in_bytes = 2 if fam == 3 else 4
+    comp_bytes = (Mr * K + K * N) * in_bytes + Mr * N * 4
+    hbm_side = {"compulsory_bytes": comp_bytes, "achieved_gbs": comp_bytes / (ms_local * 1e-3) / 1e9,
+                "peak_gbs": peaks["hbm_gbs"], "frac": comp_bytes / (ms_local * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                "t_floor_us": {"memory": comp_bytes / (peaks["hbm_gbs"] * 1e9) * 1e6,
+                               "compute": flops_rank / (peak * 1e12) * 1e6}}
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
     if os.path.exists(tp):
@@ -419,7 +429,7 @@ def main():
             "pct_of_peak": 100.0 * achieved / peak,
             "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_note,
-                         "algorithmic": f"2*M*N*K = {flops_rank:.4g} flop per launch"},
+                         "algorithmic": f"2*M*N*K = {flops_rank:.4g} flop per launch", "hbm_side": hbm_side},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": "tt_gemm_host (pinned host A,B -> device -> C host)"},

@@ -59,7 +59,8 @@ struct UmmaArgs {
 };
 
 // TT_UMMA_TRACE layout: [cluster][kTraceItems][8] u64 = tile, kb0 | kb1 << 16 | order << 32,
-// t(MMA start), t(MMA last issue), t(epilogue: accumulator ready), t(epilogue: flag ok), t(done), 0
+// t(MMA start), t(MMA last issue), t(epilogue: accumulator ready), t(epilogue: flag ok), t(done),
+// and in slot 7: kernel entry (item 0) / teardown barrier passed (item 1)
 constexpr int kTraceItems = 16;
 
 // ---------------------------------------------------------------- PTX helpers
@@ -393,6 +394,8 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
   const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
   const bool leader = rank == 0;
 
+  if (p.trace && warp == 0 && lane == 0 && leader)          // debug: kernel entry (item 0, slot 7)
+    p.trace[((int64_t)(blockIdx.x / CG) * kTraceItems) * 8 + 7] = globaltimer();
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
@@ -591,6 +594,8 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
+  if (p.trace && warp == 0 && lane == 0 && leader)          // debug: teardown reached (item 1, slot 7)
+    p.trace[((int64_t)(blockIdx.x / CG) * kTraceItems + 1) * 8 + 7] = globaltimer();
   if (warp == 2) {
     if constexpr (CG == 1)
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(p.tmem_cols));

@@ -51,7 +51,11 @@ def main():
         valid = tr[:, :, 2] > 0
         t0 = tr[:, :, 2][valid].min()
         end = tr[:, :, 6][valid].max()
-        print(f"clusters {ncl} dp_tiles {dp} sk_tiles {sk} kernel span {(end - t0) / 1e3:.2f} us")
+        entry = tr[:, 0, 7]
+        teardown = tr[:, 1, 7]
+        print(f"clusters {ncl} dp_tiles {dp} sk_tiles {sk} kernel span {(end - t0) / 1e3:.2f} us; "
+              f"entry {(entry.min() - t0) / 1e3:.2f} .. {(entry.max() - t0) / 1e3:.2f} us, "
+              f"teardown passed {(teardown.max() - t0) / 1e3:.2f} us (relative to the first MMA)")
         ends = []
         for c in range(ncl):
             items = []
