@@ -9,10 +9,11 @@
 // Cluster tile = (m1 m2 128) x (n2 n3).  C[M][N] fp32 = A[M][K] . B[K][N] with A K-major and
 // B MN-major (row-major B is read transposed by the descriptor; no copy).
 //
-// Warp roles (256 threads, 1 CTA per SM): warp 0 = TMA producer (A and B slabs into a
+// Warp roles (384 threads, 1 CTA per SM): warp 0 = TMA producer (A and B slabs into a
 // `stages`-deep shared-memory ring guarded by full/empty mbarriers), warp 1 = MMA issuer
-// (one elected thread, leader CTA only), warp 2 = TMEM allocator, warps 4-7 = epilogue
-// (TMEM -> registers via tcgen05.ld -> global fp32 C).  Accumulators are double buffered in
+// (one elected thread, leader CTA only), warp 2 = TMEM allocator, warps 4-11 = epilogue
+// (TMEM -> registers via tcgen05.ld -> swizzled smem -> TMA store of fp32 C; two warps per
+// TMEM lane quarter).  Accumulators are double buffered in
 // TMEM when m2 n2 n3 <= 256 columns so the epilogue of tile t overlaps the MMAs of tile t+1.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -32,7 +33,12 @@ namespace tt {
 
 namespace {
 
-constexpr int kEpiBytes = 32768;   // epilogue staging (the J_hw reserve)
+constexpr int kEpiBytes = 32768;   // minimum epilogue staging (the J_hw reserve)
+constexpr int kEpiBoxBytes = 4096; // one 32 x 32 fp32 staging box
+constexpr int kEpiMaxBufs = 8;     // boxes per epilogue warp
+constexpr int kEpiWarps = 8;       // warps 4 .. 11: two per TMEM lane quarter, alternating 32-column chunks
+constexpr int kThreads = 32 * (4 + kEpiWarps);
+static_assert(kEpiWarps * kEpiBoxBytes == kEpiBytes, "one box per epilogue warp fills the J_hw reserve");
 
 struct UmmaArgs {
   int64_t M, N, K;
@@ -49,6 +55,7 @@ struct UmmaArgs {
   int b_cw;                         // B columns per TMA box (swz_b / elem)
   int nb;                           // B columns per CTA per atom = n3 / cta_group
   int a_stage_bytes, stage_bytes;   // A part, total per stage (A + padded B)
+  int epi_bufs;                     // 4 KB staging boxes per epilogue warp (1 .. kEpiMaxBufs)
   uint32_t idesc;
   uint32_t tx_bytes;                // bytes landing per stage per CTA
   // tail split: the last sk_tiles tiles' k-blocks are spread evenly over the
@@ -138,6 +145,19 @@ __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target)
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+// wait until at most n bulk groups are still reading shared memory (n is warp-uniform)
+__device__ __forceinline__ void bulk_wait_read_n(int n) {
+  switch (n) {
+    case 0: bulk_wait_read<0>(); break;
+    case 1: bulk_wait_read<1>(); break;
+    case 2: bulk_wait_read<2>(); break;
+    case 3: bulk_wait_read<3>(); break;
+    case 4: bulk_wait_read<4>(); break;
+    case 5: bulk_wait_read<5>(); break;
+    case 6: bulk_wait_read<6>(); break;
+    default: bulk_wait_read<7>(); break;
+  }
+}
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
@@ -309,9 +329,13 @@ __device__ __forceinline__ void mma_role(const UmmaArgs& p, const MmaCtx& c) {
   const uint64_t b_hi = smem_desc(0, lbo_b, (uint32_t)p.sbo_b, p.b_layout) & 0xFFFFFFFF00000000ull;
   const uint32_t a_lbo = p.a_mn ? (((a_box >> 4) & 0x3FFFu) << 16) : (1u << 16);
   const uint32_t b_lbo = ((lbo_b >> 4) & 0x3FFFu) << 16;
-  uint32_t a_off[KS][M2], b_off[KS][N2], d_off[M2][N2];
+  // At most 16 k-steps are unrolled with per-step offsets in registers; a 32-step stage (tf32,
+  // BK = 256) replays them with a constant shift (+16 k-steps = +512 B along K in every layout).
+  constexpr int KSU = KS > 16 ? 16 : KS;
+  constexpr int REP = KS / KSU;
+  uint32_t a_off[KSU][M2], b_off[KSU][N2], d_off[M2][N2];
 #pragma unroll
-  for (int ks = 0; ks < KS; ++ks) {
+  for (int ks = 0; ks < KSU; ++ks) {
     const uint32_t kbytes = (uint32_t)(ks * UK * ELEM);
 #pragma unroll
     for (int mi = 0; mi < M2; ++mi)
@@ -322,6 +346,10 @@ __device__ __forceinline__ void mma_role(const UmmaArgs& p, const MmaCtx& c) {
     for (int ni = 0; ni < N2; ++ni)
       b_off[ks][ni] = (((uint32_t)(ni * (p.nb / p.b_cw)) * lbo_b + (uint32_t)(ks * UK * p.swz_b)) >> 4) | b_lbo;
   }
+  const uint32_t a_rep = (uint32_t)(p.a_mn ? (KSU * UK * 128) : ((KSU * UK * ELEM) / p.swz_a) * p.a_chunk_bytes) >> 4;
+  const uint32_t b_rep = (uint32_t)(KSU * UK * p.swz_b) >> 4;
+  (void)a_rep;
+  (void)b_rep;
 #pragma unroll
   for (int mi = 0; mi < M2; ++mi)
 #pragma unroll
@@ -348,13 +376,16 @@ __device__ __forceinline__ void mma_role(const UmmaArgs& p, const MmaCtx& c) {
       const uint32_t sb16 = sa16 + ((uint32_t)p.a_stage_bytes >> 4);
       if (elect_one()) {
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks)
+        for (int rep = 0; rep < REP; ++rep)
 #pragma unroll
-          for (int mi = 0; mi < M2; ++mi)
+          for (int ks = 0; ks < KSU; ++ks)
 #pragma unroll
-            for (int ni = 0; ni < N2; ++ni)
-              umma<KIND, CG>(dbase + d_off[mi][ni], a_hi | (uint64_t)(sa16 + a_off[ks][mi]),
-                             b_hi | (uint64_t)(sb16 + b_off[ks][ni]), p.idesc, (kb != it.kb0 || ks != 0) ? 1u : 0u);
+            for (int mi = 0; mi < M2; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < N2; ++ni)
+                umma<KIND, CG>(dbase + d_off[mi][ni], a_hi | (uint64_t)(sa16 + rep * a_rep + a_off[ks][mi]),
+                               b_hi | (uint64_t)(sb16 + rep * b_rep + b_off[ks][ni]), p.idesc,
+                               (kb != it.kb0 || rep != 0 || ks != 0) ? 1u : 0u);
         umma_commit<CG>(c.empty0 + 8u * stage);              // frees the smem slot when MMAs finish
       }
       __syncwarp();
@@ -371,7 +402,7 @@ __device__ __forceinline__ void mma_role(const UmmaArgs& p, const MmaCtx& c) {
 
 // ---------------------------------------------------------------- the kernel
 template <int KIND, int CG>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kThreads, 1)
 k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
        const __grid_constant__ CUtensorMap tmC, float* __restrict__ C,
        const UmmaArgs p) {
@@ -380,8 +411,9 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t epi_base = sbase + (uint32_t)p.stages * p.stage_bytes;   // 4 warps x 2 x 4 KB staging
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)p.stages * p.stage_bytes + kEpiBytes);
+  const uint32_t epi_base = sbase + (uint32_t)p.stages * p.stage_bytes;   // kEpiWarps x epi_bufs x 4 KB staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)p.stages * p.stage_bytes +
+                                               (size_t)kEpiWarps * p.epi_bufs * kEpiBoxBytes);
   const uint32_t full0 = smem_u32(bars);
   const uint32_t empty0 = full0 + 8u * p.stages;
   const uint32_t tfull0 = empty0 + 8u * p.stages;
@@ -408,7 +440,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull0 + 8u * b, 1);
-      mbar_init(tempty0 + 8u * b, 4 * CG);
+      mbar_init(tempty0 + 8u * b, kEpiWarps * CG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -490,11 +522,14 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     }
   } else if (warp >= 4) {
     // ===== epilogue: TMEM -> registers -> swizzled smem box -> TMA bulk store =====
-    // Each warp owns TMEM lanes [32q, 32q+32) (= 32 output rows) and two 4 KB staging boxes
-    // (32 rows x 32 fp32, 128B-swizzled like the C tensor map) used alternately; one lane
-    // issues cp.async.bulk.tensor stores, so C leaves the SM as full 128 B lines.
+    // Warps 4 .. 11: warp w reads TMEM lanes [32q, 32q+32) (q = w mod 4, 32 output rows) and
+    // takes every other 32-column chunk of the tile (h = column parity), so two independent
+    // load -> stage -> store chains run per lane quarter.  Each warp stages through its own
+    // 4 KB boxes (32 rows x 32 fp32, 128B-swizzled like the C tensor map); one lane issues the
+    // cp.async.bulk.tensor store, so C leaves the SM as full 128 B lines.
     const int q = warp & 3;
-    const uint32_t stage0 = epi_base + (uint32_t)q * 8192u;
+    const int h = (warp - 4) >> 2;
+    const uint32_t stage0 = epi_base + (uint32_t)((warp - 4) * p.epi_bufs * kEpiBoxBytes);
     int acc = 0;
     uint32_t aphase = 0;
     int sbuf = 0;
@@ -503,7 +538,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     Item it;
     int item_no = 0;
     while (sch.next(p, &it)) {
-      uint64_t* tr = (p.trace && q == 0 && lane == 0 && leader && item_no < kTraceItems)
+      uint64_t* tr = (p.trace && warp == 4 && lane == 0 && leader && item_no < kTraceItems)
                          ? p.trace + ((int64_t)cluster_id * kTraceItems + item_no) * 8 : nullptr;
       ++item_no;
       const int tm = it.tile % p.m0, tn = it.tile / p.m0;
@@ -517,11 +552,12 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
         tr[4] = globaltimer();
       }
       if (add) {
-        wait_flag(flag, 4u * (uint32_t)it.order);          // the 4 epilogue warps of each piece above
+        wait_flag(flag, (uint32_t)kEpiWarps * (uint32_t)it.order);   // every epilogue warp of each piece above
         fence_proxy_async_global();
       }
       if (tr) tr[5] = globaltimer();
       const int row_cta = tm * (CG * rows_cta) + (int)rank * rows_cta;
+      int chunk = 0;                                       // running chunk index over the tile
       for (int mi = 0; mi < p.m2; ++mi) {
         const int row0 = row_cta + mi * 128 + q * 32;
         for (int ni = 0; ni < p.n2; ++ni) {
@@ -529,10 +565,11 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
           const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + tcol;
           const int col0 = tn * (p.n2 * p.n3) + ni * p.n3;
           int c0 = 0;
-          for (; c0 + 32 <= p.n3; c0 += 32) {
+          for (; c0 + 32 <= p.n3; c0 += 32, ++chunk) {
+            if ((chunk & 1) != h) continue;
             tmem_ld32(taddr + (uint32_t)c0, v);
-            const uint32_t buf = stage0 + (uint32_t)sbuf * 4096u;
-            if (lane == 0) bulk_wait_read<1>();            // the store that used `buf` has read it
+            const uint32_t buf = stage0 + (uint32_t)(sbuf * kEpiBoxBytes);
+            if (lane == 0) bulk_wait_read_n(p.epi_bufs - 1);  // the store that used `buf` has read it
             __syncwarp();
             const uint32_t rowp = buf + (uint32_t)lane * 128u;
 #pragma unroll
@@ -545,19 +582,21 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
               else tma_store_2d(&tmC, buf, col0 + c0, row0);
               bulk_commit();
             }
-            sbuf ^= 1;
+            if (++sbuf == p.epi_bufs) sbuf = 0;
           }
           if (c0 < p.n3) {                                 // n3 = 16: direct 16-column stores
-            tmem_ld16(taddr + (uint32_t)c0, v);
-            float4* dst = reinterpret_cast<float4*>(C + (int64_t)(row0 + lane) * p.N + col0 + c0);
+            if ((chunk++ & 1) == h) {
+              tmem_ld16(taddr + (uint32_t)c0, v);
+              float4* dst = reinterpret_cast<float4*>(C + (int64_t)(row0 + lane) * p.N + col0 + c0);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              float4 o = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-              if (add) {
-                const float4 c = dst[j];
-                o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
+              for (int j = 0; j < 4; ++j) {
+                float4 o = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                if (add) {
+                  const float4 c = dst[j];
+                  o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
+                }
+                dst[j] = o;
               }
-              dst[j] = o;
             }
           }
         }
@@ -577,7 +616,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
         __syncwarp();
         if (lane == 0) {
           const uint32_t old = atom_add_release(flag, 1u);
-          if (it.kb0 == 0 && old == 4u * (uint32_t)it.order + 3u) *flag = 0u;   // last piece: reset
+          if (it.kb0 == 0 && old == (uint32_t)kEpiWarps * ((uint32_t)it.order + 1u) - 1u) *flag = 0u;   // last piece: reset
         }
       }
       if (tr) {
@@ -685,7 +724,7 @@ int query_clusters(int smem) {
   if (!set_smem_attr<KIND, CG>(&err)) return 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(num_sms() / CG * CG), 1, 1);
-  cfg.blockDim = dim3(256, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = (size_t)smem;
   cudaLaunchAttribute attrs[1];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
@@ -787,6 +826,16 @@ void plan_of(const Space& sp, const State& s, Plan* pl) {
   a.stage_bytes = (int)umma_stage_bytes(fam, s);
   a.tx_bytes = (uint32_t)(a.a_stage_bytes + a.n2 * a.nb * a.bk * elem);
   a.stages = std::min<int>(kUmmaMaxStages, kUmmaPipeSmem / a.stage_bytes);
+  // TT_UMMA_STAGES (experiments): fewer pipeline stages; the freed shared memory goes to the
+  // epilogue staging.  Leftover pipeline memory always does.
+  if (const char* e = std::getenv("TT_UMMA_STAGES")) {
+    const int want = std::atoi(e);
+    if (want >= 2 && want < a.stages) a.stages = want;
+  }
+  {
+    const int spare = kUmmaPipeSmem - a.stages * a.stage_bytes;
+    a.epi_bufs = std::min(kEpiMaxBufs, 1 + std::max(0, spare) / (kEpiWarps * kEpiBoxBytes));
+  }
   a.acc_cols = a.m2 * a.n2 * a.n3;
   a.acc_bufs = a.acc_cols <= 256 ? 2 : 1;
   int need = a.acc_cols * a.acc_bufs, cols = 32;
@@ -802,7 +851,7 @@ void plan_of(const Space& sp, const State& s, Plan* pl) {
             ((M_inst >> 4) << 24);
   pl->cg = m1;
   pl->kind = kind;
-  pl->smem = a.stages * a.stage_bytes + kEpiBytes + 1024 /*align*/ + 8 * (2 * a.stages + 4) + 16;
+  pl->smem = a.stages * a.stage_bytes + kEpiWarps * a.epi_bufs * kEpiBoxBytes + 1024 /*align*/ + 8 * (2 * a.stages + 4) + 16;
   // persistent grid: as many clusters as can be co-resident (the tail split's cross-cluster
   // waits rely on it), never more than there are tiles unless the tail is split
   const int tiles = a.m0 * a.n0;
@@ -837,7 +886,7 @@ tt_status launch_t(const Plan& pl, const CUtensorMap& ma, const CUtensorMap& mb,
   if (!set_smem_attr<KIND, CG>(err)) return TT_E_CUDA;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)pl.grid, 1, 1);
-  cfg.blockDim = dim3(256, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = (size_t)pl.smem;
   cfg.stream = stream;
   cudaLaunchAttribute attrs[1];
@@ -884,7 +933,7 @@ tt_status umma_bind(const Space& sp, const State& s, tt_launch_info* info, std::
   info->grid_x = pl.grid;
   info->grid_y = 1;
   info->grid_z = 1;
-  info->block_x = 256;
+  info->block_x = kThreads;
   info->cluster_x = pl.cg;
   info->smem_bytes = pl.smem;
   info->stages = pl.a.stages;
