@@ -36,10 +36,10 @@ def _deps_mtime() -> float:
     return max(os.path.getmtime(f) for f in files)
 
 
-def _compile(src: str) -> str:
-    obj = os.path.join(OBJ, src + ".o")
+def _compile(src: str, obj_dir: str = OBJ, defines=()) -> str:
+    obj = os.path.join(obj_dir, src + ".o")
     cmd = [nvcc(), "-c", os.path.join(SRC, src), "-o", obj, "-O3", "-std=c++17", "-lineinfo",
-           "-Xcompiler", "-fPIC", "-I", INCLUDE] + ARCH
+           "-Xcompiler", "-fPIC", "-I", INCLUDE] + ARCH + [f"-D{d}" for d in defines]
     if src.endswith(".cu"):
         cmd += ["-Xptxas", "-v"] if os.environ.get("TT_PTXAS_VERBOSE") else []
     else:   # host search code: no mul-add contraction, so the N-A2C MLP sums exactly as written (Z24)
@@ -66,5 +66,23 @@ def build(force: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines) -> str:
+    """Experiment build: the same sources with extra -D defines -> build/variants/<name>/libtiletune.so
+    (load it with TT_LIB_PATH)."""
+    obj_dir = os.path.join(HERE, "..", "build", "variants", name)
+    os.makedirs(obj_dir, exist_ok=True)
+    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, obj_dir, defines), SOURCES))
+    lib = os.path.join(obj_dir, "libtiletune.so")
+    r = subprocess.run([nvcc(), "-shared", "-o", lib] + objs + ARCH + ["-lpthread"], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed:\n{r.stderr}")
+    return lib
+
+
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv))
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        print(build_variant(sys.argv[i + 1], sys.argv[i + 2:]))
+    else:
+        print(build(force="--force" in sys.argv))

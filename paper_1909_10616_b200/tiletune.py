@@ -13,7 +13,8 @@ import os
 from typing import Callable, List, Optional, Sequence, Tuple
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtiletune.so")
+# TT_LIB_PATH: an alternative in-tree build of the same sources (kernel A/B experiments)
+LIB_PATH = os.environ.get("TT_LIB_PATH") or os.path.join(HERE, "libtiletune.so")
 
 OK, E_INVAL, E_ILLEGITIMATE, E_INFEASIBLE, E_OVERFLOW, E_CAPACITY, E_CUDA, E_EVALUATOR, E_UNSUPPORTED = range(9)
 FAM_NONE, FAM_F32_SIMT, FAM_TF32_UMMA, FAM_BF16_UMMA = 0, 1, 2, 3

@@ -1,4 +1,6 @@
-# small-shape runs of every kernel family for compute-sanitizer
+# small-shape runs of every kernel family for compute-sanitizer (plain, then the tcgen05 tail
+# split forced on, then graph-replayed measurements)
+import os
 import sys
 sys.path.insert(0, '.')
 import torch
@@ -16,6 +18,24 @@ for fam, n, cfgs in [(1, 128, [((2, 2, 8, 4), (16, 8), (2, 2, 4, 8)), ((128, 1, 
         torch.cuda.synchronize()
         ref = A.float() @ B.float()
         print(fam, s, float((C - ref).abs().max() / ref.abs().max()))
+os.environ["TT_TAIL_SPLIT"] = "2"        # every UMMA config with tiles % clusters != 0 splits
+for fam, n, cfgs in [(3, 512, [((4, 1, 1, 128), (8, 64), (4, 1, 1, 128)), ((2, 2, 1, 128), (32, 16), (16, 1, 1, 32))]),
+                     (2, 256, [((2, 1, 1, 128), (8, 32), (2, 1, 1, 128))])]:
+    dt = torch.bfloat16 if fam == 3 else torch.float32
+    A = torch.randn(n, n, device=dev).to(dt)
+    B = torch.randn(n, n, device=dev).to(dt)
+    C = torch.empty(n, n, device=dev)
+    for s in cfgs:
+        info = tt.binding(tt.make_space(n, n, n, family=fam), s)
+        for _ in range(2):
+            tt.gemm(A, B, C, fam, s)
+        torch.cuda.synchronize()
+        ref = A.float() @ B.float()
+        print("split", info.split_tiles, fam, s, float((C - ref).abs().max() / ref.abs().max()))
+del os.environ["TT_TAIL_SPLIT"]
 ctx = tt.Context(0)
+smp = ctx.measure(tt.make_space(512, 512, 512, family=3), ((4, 1, 1, 128), (8, 64), (4, 1, 1, 128)),
+                  tt.measure_opts(repeats=2))
+print("graph measure ok", smp.graph_nodes, smp.number)
 res = tt.gbfs_search(128, 128, 128, 8, tt.search_opts(family=1, seed=0, measure={"repeats": 2}), ctx=ctx)
 print("search ok", res.evals)
