@@ -191,7 +191,8 @@ struct Mlp {
   void backward(const std::vector<std::vector<double>>& acts, const double* dout,
                 std::vector<std::vector<double>>& gW, std::vector<std::vector<double>>& gb) const {
     const int L = layers();
-    std::vector<double> d(dout, dout + sz[L]), dn;
+    std::vector<double> d((size_t)sz[L]), dn;
+    for (int i = 0; i < sz[L]; ++i) d[i] = dout[i];
     for (int l = L - 1; l >= 0; --l) {
       const int fi = sz[l], fo = sz[l + 1];
       for (int r = 0; r < fo; ++r) {
