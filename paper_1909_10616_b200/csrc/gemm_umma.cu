@@ -9,11 +9,10 @@
 // Cluster tile = (m1 m2 128) x (n2 n3).  C[M][N] fp32 = A[M][K] . B[K][N] with A K-major and
 // B MN-major (row-major B is read transposed by the descriptor; no copy).
 //
-// Warp roles (384 threads, 1 CTA per SM): warp 0 = TMA producer (A and B slabs into a
+// Warp roles (256 threads, 1 CTA per SM): warp 0 = TMA producer (A and B slabs into a
 // `stages`-deep shared-memory ring guarded by full/empty mbarriers), warp 1 = MMA issuer
-// (one elected thread, leader CTA only), warp 2 = TMEM allocator, warps 4-11 = epilogue
-// (TMEM -> registers via tcgen05.ld -> swizzled smem -> TMA store of fp32 C; two warps per
-// TMEM lane quarter).  Accumulators are double buffered in
+// (one elected thread, leader CTA only), warp 2 = TMEM allocator, warps 4-7 = epilogue
+// (TMEM -> registers via tcgen05.ld -> swizzled smem -> TMA store of fp32 C).  Accumulators are double buffered in
 // TMEM when m2 n2 n3 <= 256 columns so the epilogue of tile t overlaps the MMAs of tile t+1.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -36,9 +35,14 @@ namespace {
 constexpr int kEpiBytes = 32768;   // minimum epilogue staging (the J_hw reserve)
 constexpr int kEpiBoxBytes = 4096; // one 32 x 32 fp32 staging box
 constexpr int kEpiMaxBufs = 8;     // boxes per epilogue warp
-constexpr int kEpiWarps = 8;       // warps 4 .. 11: two per TMEM lane quarter, alternating 32-column chunks
+// Epilogue warps 4 .. 3 + kEpiWarps; kEpiWarps / 4 warps per TMEM lane quarter take its 32-column
+// chunks round-robin.  8 warps measured no faster than 4 (the SM's write path bounds the drain,
+// profiles/r3_epilogue.md) and cost ~3 % at 4096^3 by competing with the MMA phase for shared
+// memory, so 4.
+constexpr int kEpiWarps = 4;
+constexpr int kEpiGroups = kEpiWarps / 4;
 constexpr int kThreads = 32 * (4 + kEpiWarps);
-static_assert(kEpiWarps * kEpiBoxBytes == kEpiBytes, "one box per epilogue warp fills the J_hw reserve");
+static_assert(kEpiWarps % 4 == 0 && kEpiWarps * kEpiBoxBytes <= kEpiBytes, "the epilogue staging fits the J_hw reserve");
 
 struct UmmaArgs {
   int64_t M, N, K;
@@ -522,9 +526,8 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     }
   } else if (warp >= 4) {
     // ===== epilogue: TMEM -> registers -> swizzled smem box -> TMA bulk store =====
-    // Warps 4 .. 11: warp w reads TMEM lanes [32q, 32q+32) (q = w mod 4, 32 output rows) and
-    // takes every other 32-column chunk of the tile (h = column parity), so two independent
-    // load -> stage -> store chains run per lane quarter.  Each warp stages through its own
+    // Warp w reads TMEM lanes [32q, 32q+32) (q = w mod 4, 32 output rows) and takes the
+    // 32-column chunks of the tile with index = h mod kEpiGroups.  Each warp stages through its own
     // 4 KB boxes (32 rows x 32 fp32, 128B-swizzled like the C tensor map); one lane issues the
     // cp.async.bulk.tensor store, so C leaves the SM as full 128 B lines.
     const int q = warp & 3;
@@ -566,7 +569,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
           const int col0 = tn * (p.n2 * p.n3) + ni * p.n3;
           int c0 = 0;
           for (; c0 + 32 <= p.n3; c0 += 32, ++chunk) {
-            if ((chunk & 1) != h) continue;
+            if (chunk % kEpiGroups != h) continue;
             tmem_ld32(taddr + (uint32_t)c0, v);
             const uint32_t buf = stage0 + (uint32_t)(sbuf * kEpiBoxBytes);
             if (lane == 0) bulk_wait_read_n(p.epi_bufs - 1);  // the store that used `buf` has read it
@@ -585,7 +588,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             if (++sbuf == p.epi_bufs) sbuf = 0;
           }
           if (c0 < p.n3) {                                 // n3 = 16: direct 16-column stores
-            if ((chunk++ & 1) == h) {
+            if (chunk++ % kEpiGroups == h) {
               tmem_ld16(taddr + (uint32_t)c0, v);
               float4* dst = reinterpret_cast<float4*>(C + (int64_t)(row0 + lane) * p.N + col0 + c0);
 #pragma unroll
@@ -834,7 +837,7 @@ void plan_of(const Space& sp, const State& s, Plan* pl) {
   }
   {
     const int spare = kUmmaPipeSmem - a.stages * a.stage_bytes;
-    a.epi_bufs = std::min(kEpiMaxBufs, 1 + std::max(0, spare) / (kEpiWarps * kEpiBoxBytes));
+    a.epi_bufs = std::min(kEpiMaxBufs, kEpiBytes / (kEpiWarps * kEpiBoxBytes) + std::max(0, spare) / (kEpiWarps * kEpiBoxBytes));
   }
   a.acc_cols = a.m2 * a.n2 * a.n3;
   a.acc_bufs = a.acc_cols <= 256 ? 2 : 1;
