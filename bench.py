@@ -297,6 +297,20 @@ def main():
                 "frac_feasible": res.frac_feasible, "tuning_wall_s": tune_wall, "best_config": best,
                 "best_cost_us": res.best_cost * 1e6, "s0_cost_us": res.trace[0]["cost"] * 1e6,
                 "local_evals": ev.local_evals}
+        if world == 1:
+            # Projection of the sharded search from this run's per-candidate
+            # measurement times: candidate j of a round on rank j mod G, the slowest rank gates
+            # the round, + 50 us per round for the all_gather; the host search work is
+            # replicated on every rank.  Not a multi-GPU measurement (the driver's N = 2/4/8 runs
+            # measure tuning_wall_s directly).
+            meas = sum(sum(t) for t in ev.round_times)
+            host = max(0.0, tune_wall - meas)
+            proj = {}
+            for G in (2, 4, 8):
+                w = host + tdist.projected_sharded_wall(ev.round_times, G, per_round_s=50e-6)
+                proj[str(G)] = {"wall_s": w, "speedup": tune_wall / w if w > 0 else None}
+            tune["projected_sharded_search"] = {"rounds": ev.rounds, "measure_s": meas, "host_s": host,
+                                                "by_gpus": proj, "kind": "projection from 1-GPU per-candidate times"}
     info = tt.binding(sp, best)
 
     # ---------------- 2. timed steps of the best-found GEMM on this rank's row shard ----------

@@ -15,6 +15,7 @@ libtiletune call.
 from __future__ import annotations
 
 import math
+import time
 from typing import Callable, List, Optional, Sequence
 
 import torch
@@ -39,13 +40,18 @@ class ShardedEvaluator:
         self.device = device or torch.device("cpu")
         self.rounds = 0
         self.local_evals = 0
+        self.round_times: List[List[float]] = []   # per round: wall time of each local measurement
 
     def __call__(self, states: Sequence) -> List[float]:
         n = len(states)
         mine = torch.zeros(n, dtype=torch.float64, device=self.device)
+        times = [0.0] * n
         for j in range(self.rank, n, self.world):
+            t0 = time.perf_counter()
             mine[j] = float(self.measure_one(states[j]))
+            times[j] = time.perf_counter() - t0
             self.local_evals += 1
+        self.round_times.append(times)
         self.rounds += 1
         if self.world == 1:
             return mine.tolist()
@@ -75,6 +81,20 @@ def device_measure(ctx: tt.Context, sp: tt.Space, opts: Optional[tt.MeasureOpts]
             state["best"] = min(state["best"], c)
 
     return f, observe
+
+
+def projected_sharded_wall(round_times: Sequence[Sequence[float]], world: int, per_round_s: float = 0.0) -> float:
+    """Measurement wall time of the same traversal sharded over ``world`` ranks (candidate j on
+    rank j mod world), from per-candidate times recorded on one rank: sum over rounds of the
+    slowest rank's share, plus ``per_round_s`` (the all_gather) per round.  A projection from
+    measured times, not a multi-GPU measurement."""
+    total = 0.0
+    for times in round_times:
+        share = [0.0] * world
+        for j, t in enumerate(times):
+            share[j % world] += t
+        total += max(share) + (per_round_s if world > 1 else 0.0)
+    return total
 
 
 class TrackingEvaluator(ShardedEvaluator):

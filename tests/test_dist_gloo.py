@@ -9,6 +9,7 @@ import torch.multiprocessing as mp
 
 from oracle import costs, gbfs as ogbfs, na2c as ona2c, space
 from oracle.space import Spec
+from paper_1909_10616_b200 import dist as tdist
 
 
 def _free_port():
@@ -64,3 +65,10 @@ def test_sharded_search_matches_oracle(algo):
     assert n0 + n1 == len(ref)                             # each candidate measured exactly once
     assert abs(n0 - n1) <= rounds0                         # round-robin balance
     assert rr0 == (0, 4096) and rr1 == (4096, 8192)        # exact row partition
+
+def test_projection():
+    rt = [[1.0], [1.0, 2.0, 3.0, 4.0], [0.5] * 8]
+    assert tdist.projected_sharded_wall(rt, 1) == 1.0 + 10.0 + 4.0
+    # G = 2: round 2 shares (1+3, 2+4) -> 6; round 3 -> 2.0
+    assert tdist.projected_sharded_wall(rt, 2) == 1.0 + 6.0 + 2.0
+    assert tdist.projected_sharded_wall(rt, 8, per_round_s=0.1) == 1.1 + 4.1 + 0.6
