@@ -81,7 +81,7 @@ def j_hw(spec, s) -> bool:
         elem = _elem_bytes(fam)
         if m3 != UMMA_M_ATOM or m1 not in (1, 2) or m2 not in (1, 2):
             return False
-        if n1 != 1 or n2 not in (1, 2):
+        if n1 not in (1, 2) or n2 not in (1, 2):      # n1 = clusters of n1 pairs sharing A (multicast)
             return False
         if n3 % 16 != 0 or not (16 <= n3 <= 256):
             return False

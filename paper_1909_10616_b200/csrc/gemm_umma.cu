@@ -60,6 +60,8 @@ struct UmmaArgs {
   int nb;                           // B columns per CTA per atom = n3 / cta_group
   int a_stage_bytes, stage_bytes;   // A part, total per stage (A + padded B)
   int epi_bufs;                     // 4 KB staging boxes per epilogue warp (1 .. kEpiMaxBufs)
+  int n1;                           // CTA pairs (or CTAs) per cluster along N; 2 = A multicast
+  int a_box_rows;                   // K-major A: rows per TMA box (m2 128 / n1: each pair loads its share)
   uint32_t idesc;
   uint32_t tx_bytes;                // bytes landing per stage per CTA
   // tail split: the last sk_tiles tiles' k-blocks are spread evenly over the
@@ -191,6 +193,24 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint32_t bar
   }
 }
 
+// Multicast load: the box lands at the same shared-memory offset in every CTA of `mask` and
+// each destination's pair leader (peer bit cleared for cta_group::2) receives the complete_tx.
+template <int CG>
+__device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, uint32_t bar, uint32_t dst, int x, int y,
+                                               uint16_t mask) {
+  if constexpr (CG == 1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%2, %3}], [%4], %5;"
+        ::"r"(dst), "l"(map), "r"(x), "r"(y), "r"(bar), "h"(mask) : "memory");
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%2, %3}], [%4], %5;"
+        ::"r"(dst), "l"(map), "r"(x), "r"(y), "r"(bar & 0xFEFFFFFFu), "h"(mask) : "memory");
+  }
+}
+
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, int layout_code) {
   // tcgen05 shared-memory matrix descriptor: start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46),
   // version 1 [46,48), base offset 0, layout [61,64): SW128 = 2, SW64 = 4, SW32 = 6,
@@ -220,13 +240,19 @@ __device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t a, uint64_t b, ui
                  ::"r"(d_tmem), "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
+// Arrive (when the issued MMAs complete) on `bar` in every CTA of `mask`; mask 0 = this CTA only.
 template <int CG>
-__device__ __forceinline__ void umma_commit(uint32_t bar) {
-  if constexpr (CG == 1)
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
-  else
+__device__ __forceinline__ void umma_commit(uint32_t bar, uint16_t mask) {
+  if constexpr (CG == 1) {
+    if (mask == 0)
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+    else
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                   ::"r"(bar), "h"(mask) : "memory");
+  } else {
     asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
-                 ::"r"(bar), "h"((uint16_t)0x3) : "memory");
+                 ::"r"(bar), "h"(mask) : "memory");
+  }
 }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -317,6 +343,7 @@ struct Sched {
 struct MmaCtx {
   uint32_t sbase, full0, empty0, tfull0, tempty0, tmem_base;
   int cluster_id, num_clusters;
+  uint16_t empty_mask, tfull_mask;   // CTAs whose empty / accumulator-ready barriers a commit feeds
 };
 
 template <int KIND, int CG, int KS, int M2, int N2>
@@ -376,7 +403,9 @@ __device__ __forceinline__ void mma_role(const UmmaArgs& p, const MmaCtx& c) {
     for (int kb = it.kb0; kb < it.kb1; ++kb) {
       mbar_wait(c.full0 + 8u * stage, phase);
       tc_fence_after();
-      const uint32_t sa16 = (c.sbase + (uint32_t)stage * p.stage_bytes) >> 4;
+      // descriptor start field = CTA-window byte address >> 4 (14 bits): the cvta result of a CTA
+      // with cluster rank > 0 carries the rank above bit 24, which must not leak into LBO
+      const uint32_t sa16 = ((c.sbase + (uint32_t)stage * p.stage_bytes) >> 4) & 0x3FFFu;
       const uint32_t sb16 = sa16 + ((uint32_t)p.a_stage_bytes >> 4);
       if (elect_one()) {
 #pragma unroll
@@ -390,13 +419,13 @@ __device__ __forceinline__ void mma_role(const UmmaArgs& p, const MmaCtx& c) {
                 umma<KIND, CG>(dbase + d_off[mi][ni], a_hi | (uint64_t)(sa16 + rep * a_rep + a_off[ks][mi]),
                                b_hi | (uint64_t)(sb16 + rep * b_rep + b_off[ks][ni]), p.idesc,
                                (kb != it.kb0 || rep != 0 || ks != 0) ? 1u : 0u);
-        umma_commit<CG>(c.empty0 + 8u * stage);              // frees the smem slot when MMAs finish
+        umma_commit<CG>(c.empty0 + 8u * stage, c.empty_mask);  // frees the slot in every CTA that fills it
       }
       __syncwarp();
       if (++stage == p.stages) { stage = 0; phase ^= 1u; }
     }
     if (elect_one()) {
-      umma_commit<CG>(c.tfull0 + 8u * acc);                 // accumulator ready for the epilogue
+      umma_commit<CG>(c.tfull0 + 8u * acc, c.tfull_mask);   // accumulator ready for the epilogue
       if (tr) tr[3] = globaltimer();
     }
     __syncwarp();
@@ -427,8 +456,15 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
   // warp index made provably warp-uniform so role loops run on the uniform datapath
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
-  const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+  // cluster = n1 pairs (CG = 2) or n1 CTAs (CG = 1) side by side along N; they share A rows,
+  // so with n1 = 2 each loads its half of the A slab and multicasts it to its counterpart
+  const int csize = CG * p.n1;
+  const uint32_t crank = csize > 1 ? cluster_rank() : 0u;
+  const uint32_t rank = crank % CG;                 // CTA within the pair
+  const uint32_t pj = crank / CG;                   // pair (or CTA) index along N
   const bool leader = rank == 0;
+  const uint16_t all_mask = (uint16_t)((1u << csize) - 1u);
+  const uint16_t pair_mask = (uint16_t)(((1u << CG) - 1u) << (pj * CG));
 
   if (p.trace && warp == 0 && lane == 0 && leader)          // debug: kernel entry (item 0, slot 7)
     p.trace[((int64_t)(blockIdx.x / CG) * kTraceItems) * 8 + 7] = globaltimer();
@@ -440,7 +476,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(full0 + 8u * s, 1);     // leader arms with both CTAs' bytes
-      mbar_init(empty0 + 8u * s, 1);
+      mbar_init(empty0 + 8u * s, (uint32_t)p.n1);   // one MMA commit from each pair reading this slot
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull0 + 8u * b, 1);
@@ -458,12 +494,12 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     }
   }
   tc_fence_before();
-  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  if (csize > 1) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int cluster_id = blockIdx.x / CG;
-  const int num_clusters = gridDim.x / CG;
+  const int cluster_id = blockIdx.x / csize;
+  const int num_clusters = gridDim.x / csize;
   const int rows_cta = p.m2 * 128;
 
   if (warp == 0) {
@@ -479,7 +515,8 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     while (sch.next(p, &it)) {
       const int tm = it.tile % p.m0, tn = it.tile / p.m0;
       const int row = tm * (CG * rows_cta) + (int)rank * rows_cta;
-      const int colt = tn * (p.n2 * p.n3) + (int)rank * p.nb;
+      const int colt = tn * (p.n1 * p.n2 * p.n3) + (int)pj * (p.n2 * p.n3) + (int)rank * p.nb;
+      const uint16_t a_mask = (uint16_t)((1u << rank) | (1u << (rank + CG)));   // n1 = 2: both pairs
       for (int kb = it.kb0; kb < it.kb1; ++kb) {
         mbar_wait(empty0 + 8u * stage, phase ^ 1u);
         const uint32_t fb = full0 + 8u * stage;
@@ -488,11 +525,20 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
           const uint32_t sa = sbase + (uint32_t)stage * p.stage_bytes;
           const uint32_t sb = sa + p.a_stage_bytes;
           if (p.a_mn) {                                    // W rows: boxes of a_cw M-elements x BK
-            for (int c = 0; c < rows_cta / p.a_cw; ++c)
-              tma_load_2d<CG>(&tmA, fb, sa + (uint32_t)c * (uint32_t)(p.bk * 128), row + c * p.a_cw, kb * p.bk);
+            for (int c = 0; c < rows_cta / p.a_cw; ++c) {
+              const uint32_t dst = sa + (uint32_t)c * (uint32_t)(p.bk * 128);
+              if (p.n1 == 1) tma_load_2d<CG>(&tmA, fb, dst, row + c * p.a_cw, kb * p.bk);
+              else if ((c & 1) == (int)pj) tma_load_2d_mc<CG>(&tmA, fb, dst, row + c * p.a_cw, kb * p.bk, a_mask);
+            }
           } else {
-            for (int kc = 0; kc < kchunks; ++kc)
-              tma_load_2d<CG>(&tmA, fb, sa + kc * p.a_chunk_bytes, kb * p.bk + kc * a_kstep, row);
+            for (int kc = 0; kc < kchunks; ++kc) {
+              if (p.n1 == 1) {
+                tma_load_2d<CG>(&tmA, fb, sa + kc * p.a_chunk_bytes, kb * p.bk + kc * a_kstep, row);
+              } else {                                     // rows [pj h, pj h + h) of the slab, h = a_box_rows
+                tma_load_2d_mc<CG>(&tmA, fb, sa + kc * p.a_chunk_bytes + (uint32_t)((int)pj * p.a_box_rows * p.swz_a),
+                                   kb * p.bk + kc * a_kstep, row + (int)pj * p.a_box_rows, a_mask);
+              }
+            }
           }
           for (int ni = 0; ni < p.n2; ++ni)
             for (int c = 0; c < bboxes; ++c)
@@ -509,7 +555,8 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
       // MMA sequence is fully unrolled with loop-invariant descriptor words (issue stays far
       // below the 64-128 cycles one MMA occupies the tensor pipe).
       const int code = (p.bk / UK) * 4 + (p.m2 - 1) * 2 + (p.n2 - 1);
-      MmaCtx c{sbase, full0, empty0, tfull0, tempty0, tmem_base, cluster_id, num_clusters};
+      MmaCtx c{sbase, full0, empty0, tfull0, tempty0, tmem_base, cluster_id, num_clusters,
+               (uint16_t)(csize > 1 ? all_mask : 0), (uint16_t)(CG == 2 ? pair_mask : 0)};
       switch (code) {
 #define TT_MMA_CASE(KS, M2, N2) \
   case KS * 4 + (M2 - 1) * 2 + (N2 - 1): mma_role<KIND, CG, KS, M2, N2>(p, c); break;
@@ -545,7 +592,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                          ? p.trace + ((int64_t)cluster_id * kTraceItems + item_no) * 8 : nullptr;
       ++item_no;
       const int tm = it.tile % p.m0, tn = it.tile / p.m0;
-      uint32_t* flag = it.split ? p.flags + (it.tile - p.dp_tiles) * CG + rank : nullptr;
+      uint32_t* flag = it.split ? p.flags + (it.tile - p.dp_tiles) * csize + crank : nullptr;
       const bool add = it.split && it.order > 0;           // lower k-blocks: add onto C
       mbar_wait(tfull0 + 8u * acc, aphase);
       tc_fence_after();
@@ -566,7 +613,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
         for (int ni = 0; ni < p.n2; ++ni) {
           const uint32_t tcol = (uint32_t)(acc * p.acc_cols + (mi * p.n2 + ni) * p.n3);
           const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + tcol;
-          const int col0 = tn * (p.n2 * p.n3) + ni * p.n3;
+          const int col0 = tn * (p.n1 * p.n2 * p.n3) + (int)pj * (p.n2 * p.n3) + ni * p.n3;
           int c0 = 0;
           for (; c0 + 32 <= p.n3; c0 += 32, ++chunk) {
             if (chunk % kEpiGroups != h) continue;
@@ -608,7 +655,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
       __syncwarp();
       if (lane == 0) {                                     // TMEM drained: MMA may reuse `acc`
         if (CG == 1 || leader) mbar_arrive(tempty0 + 8u * acc);
-        else mbar_arrive_cluster(tempty0 + 8u * acc, 0);
+        else mbar_arrive_cluster(tempty0 + 8u * acc, pj * CG);
       }
       if (it.split) {                                      // publish this piece
         if (lane == 0) {
@@ -634,7 +681,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
 
   __syncwarp();                                            // reconverge role warps
   tc_fence_before();
-  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  if (csize > 1) cluster_sync(); else __syncthreads();
   tc_fence_after();
   if (p.trace && warp == 0 && lane == 0 && leader)          // debug: teardown reached (item 1, slot 7)
     p.trace[((int64_t)(blockIdx.x / CG) * kTraceItems + 1) * 8 + 7] = globaltimer();
@@ -722,16 +769,16 @@ bool set_smem_attr(std::string* err) {
 }
 
 template <int KIND, int CG>
-int query_clusters(int smem) {
+int query_clusters(int smem, int csize) {
   std::string err;
   if (!set_smem_attr<KIND, CG>(&err)) return 0;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(num_sms() / CG * CG), 1, 1);
+  cfg.gridDim = dim3((unsigned)(num_sms() / csize * csize), 1, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = (size_t)smem;
   cudaLaunchAttribute attrs[1];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
-  attrs[0].val.clusterDim.x = CG;
+  attrs[0].val.clusterDim.x = csize;
   attrs[0].val.clusterDim.y = 1;
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
@@ -746,22 +793,22 @@ int query_clusters(int smem) {
 
 // Co-resident clusters of one CTA (1 CTA per SM: launch bounds, TMEM and smem); without a
 // device (build host) the SM count.
-int max_active_clusters(int kind, int cg, int smem) {
+int max_active_clusters(int kind, int cg, int csize, int smem) {
   static std::mutex mu;
-  static std::map<std::tuple<int, int, int, int>, int> cache;
+  static std::map<std::tuple<int, int, int, int, int>, int> cache;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) {
     cudaGetLastError();
-    return num_sms() / cg;
+    return num_sms() / csize;
   }
   std::lock_guard<std::mutex> lk(mu);
-  const auto key = std::make_tuple(dev, kind, cg, smem);
+  const auto key = std::make_tuple(dev, kind, cg, csize, smem);
   auto itc = cache.find(key);
   if (itc != cache.end()) return itc->second;
-  int n = kind == 0 ? (cg == 1 ? query_clusters<0, 1>(smem) : query_clusters<0, 2>(smem))
-                    : (cg == 1 ? query_clusters<1, 1>(smem) : query_clusters<1, 2>(smem));
-  if (n <= 0) n = num_sms() / cg;
-  n = std::min(n, num_sms() / cg);
+  int n = kind == 0 ? (cg == 1 ? query_clusters<0, 1>(smem, csize) : query_clusters<0, 2>(smem, csize))
+                    : (cg == 1 ? query_clusters<1, 1>(smem, csize) : query_clusters<1, 2>(smem, csize));
+  if (n <= 0) n = num_sms() / csize;
+  n = std::min(n, num_sms() / csize);
   cache[key] = n;
   return n;
 }
@@ -788,7 +835,7 @@ uint32_t* split_flags(cudaStream_t stream, std::string* err) {
 
 struct Plan {
   UmmaArgs a;
-  int cg, kind;
+  int cg, csize, kind;    // cta_group, CTAs per cluster (cta_group x n1)
   int grid;
   int smem;
 };
@@ -808,6 +855,7 @@ void plan_of(const Space& sp, const State& s, Plan* pl) {
   a.k0 = (int)s.f[1][0];
   a.bk = (int)s.f[1][1];
   a.n0 = (int)s.f[2][0];
+  a.n1 = (int)s.f[2][1];
   a.n2 = (int)s.f[2][2];
   a.n3 = (int)s.f[2][3];
   a.nb = a.n3 / m1;
@@ -825,6 +873,7 @@ void plan_of(const Space& sp, const State& s, Plan* pl) {
     a.sbo_b = 8 * a.swz_b;
   }
   a.a_chunk_bytes = a.m2 * 128 * a.swz_a;
+  a.a_box_rows = a.m2 * 128 / a.n1;
   a.a_stage_bytes = a.m2 * 128 * a.bk * elem;
   a.stage_bytes = (int)umma_stage_bytes(fam, s);
   a.tx_bytes = (uint32_t)(a.a_stage_bytes + a.n2 * a.nb * a.bk * elem);
@@ -853,12 +902,13 @@ void plan_of(const Space& sp, const State& s, Plan* pl) {
   a.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)a.a_mn << 15) | (1u << 16) | (((uint32_t)a.n3 >> 3) << 17) |
             ((M_inst >> 4) << 24);
   pl->cg = m1;
+  pl->csize = m1 * a.n1;
   pl->kind = kind;
   pl->smem = a.stages * a.stage_bytes + kEpiWarps * a.epi_bufs * kEpiBoxBytes + 1024 /*align*/ + 8 * (2 * a.stages + 4) + 16;
   // persistent grid: as many clusters as can be co-resident (the tail split's cross-cluster
   // waits rely on it), never more than there are tiles unless the tail is split
   const int tiles = a.m0 * a.n0;
-  const int P = max_active_clusters(kind, m1, pl->smem);
+  const int P = max_active_clusters(kind, m1, pl->csize, pl->smem);
   a.dp_tiles = tiles;
   // Split only where it measured a win (profiles/r3_tail_split.md): at least one full
   // data-parallel wave behind which the pieces' extra epilogues (store, then reduce-add chain)
@@ -866,8 +916,8 @@ void plan_of(const Space& sp, const State& s, Plan* pl) {
   // previous piece's whole epilogue), and an estimated saving of >= 8 us (the idle fraction of
   // the last wave x one tile's MMA time at ~8192 (bf16) / 4096 (tf32) flop/clk/SM, 1.9 GHz).
   const int rem = tiles % P;
-  const double tile_us = 2.0 * (128.0 * m1 * a.m2) * (double)(a.n2 * a.n3) * (double)a.K /
-                         ((kind == 0 ? 8192.0 : 4096.0) * m1 * 1.9e3);
+  const double tile_us = 2.0 * (128.0 * m1 * a.m2) * (double)(a.n1 * a.n2 * a.n3) * (double)a.K /
+                         ((kind == 0 ? 8192.0 : 4096.0) * pl->csize * 1.9e3);
   const double gain_us = (1.0 - (double)rem / P) * tile_us;
   const int mode = tail_split_mode();
   const bool worth = tiles - rem >= P && a.acc_bufs == 2 && gain_us >= 8.0;
@@ -875,9 +925,9 @@ void plan_of(const Space& sp, const State& s, Plan* pl) {
     a.sk_tiles = tiles % P;                              // == tiles when tiles < P
     a.dp_tiles = tiles - a.sk_tiles;
     a.sk_workers = std::min(P, a.sk_tiles * kMaxPieces);
-    pl->grid = P * m1;
+    pl->grid = P * pl->csize;
   } else {
-    pl->grid = std::min(tiles, P) * m1;
+    pl->grid = std::min(tiles, P) * pl->csize;
   }
 }
 
@@ -894,7 +944,7 @@ tt_status launch_t(const Plan& pl, const CUtensorMap& ma, const CUtensorMap& mb,
   cfg.stream = stream;
   cudaLaunchAttribute attrs[1];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
-  attrs[0].val.clusterDim.x = CG;
+  attrs[0].val.clusterDim.x = pl.csize;
   attrs[0].val.clusterDim.y = 1;
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
@@ -937,11 +987,11 @@ tt_status umma_bind(const Space& sp, const State& s, tt_launch_info* info, std::
   info->grid_y = 1;
   info->grid_z = 1;
   info->block_x = kThreads;
-  info->cluster_x = pl.cg;
+  info->cluster_x = pl.csize;
   info->smem_bytes = pl.smem;
   info->stages = pl.a.stages;
   info->tile_m = pl.cg * pl.a.m2 * 128;
-  info->tile_n = pl.a.n2 * pl.a.n3;
+  info->tile_n = pl.a.n1 * pl.a.n2 * pl.a.n3;
   info->tile_k = pl.a.bk;
   info->tmem_cols = pl.a.tmem_cols;
   info->acc_buffers = pl.a.acc_bufs;
@@ -990,7 +1040,7 @@ tt_status prepare(const Space& sp, const State& s, const void* A, const void* B,
                   pl.kind == 1 ? -128 : 128, err))
       return TT_E_CUDA;
   } else if (!make_map(&e->ma, pl.kind, A, (uint64_t)pl.a.K, (uint64_t)pl.a.M, (uint32_t)(pl.a.swz_a / elem),
-                       (uint32_t)(pl.a.m2 * 128), pl.a.swz_a, err)) {
+                       (uint32_t)pl.a.a_box_rows, pl.a.swz_a, err)) {
     return TT_E_CUDA;
   }
   if (!make_map(&e->mb, pl.kind, B, (uint64_t)pl.a.N, (uint64_t)pl.a.K, (uint32_t)pl.a.b_cw, (uint32_t)pl.a.bk,

@@ -156,7 +156,8 @@ bool Space::j_hw(const State& s) const {
   }
   if (family == TT_FAM_TF32_UMMA || family == TT_FAM_BF16_UMMA) {
     if (m3 != 128 || (m1 != 1 && m1 != 2) || (m2 != 1 && m2 != 2)) return false;
-    if (n1 != 1 || (n2 != 1 && n2 != 2)) return false;
+    // n1 = CTA pairs per cluster along N sharing A through TMA multicast (cluster m1 n1 <= 4)
+    if ((n1 != 1 && n1 != 2) || (n2 != 1 && n2 != 2)) return false;
     if (n3 % 16 != 0 || n3 < 16 || n3 > 256) return false;
     const int64_t nb = n3 / m1;
     // MN-major B atom: >= 32 B (bf16); tf32 MN-major only as 128B swizzle with 32B atoms

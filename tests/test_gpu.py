@@ -167,7 +167,8 @@ def test_bf16_4096_sampled():
     rows = np.array([0, 129, 2048, 4095])
     R = og.gemm_f64_rows(A, B, rows)
     for s in [hw.default_s0(Spec(M, K, N, family=3)), ((16, 1, 2, 128), (64, 64), (16, 1, 1, 256)),
-              ((8, 2, 2, 128), (64, 64), (16, 1, 1, 256)), ((16, 2, 1, 128), (32, 128), (32, 1, 1, 128))]:
+              ((8, 2, 2, 128), (64, 64), (16, 1, 1, 256)), ((16, 2, 1, 128), (32, 128), (32, 1, 1, 128)),
+              ((16, 2, 1, 128), (32, 128), (8, 2, 1, 256)), ((16, 1, 2, 128), (64, 64), (8, 2, 1, 256))]:
         C = run(3, s, A, B)
         assert og.normwise_error(C[rows], R) <= 5e-3, s
         ii = np.array([5, 1000, 3000, 4095])
@@ -182,6 +183,8 @@ def test_bf16_4096_sampled():
     (3, ((16, 1, 1, 128), (32, 16), (128, 1, 1, 16))),    # n3 = 16: direct-store epilogue adds
     (2, ((16, 1, 1, 128), (16, 32), (16, 1, 1, 128))),    # tf32
     (2, ((8, 2, 1, 128), (64, 8), (16, 1, 1, 128))),
+    (3, ((8, 2, 1, 128), (8, 64), (4, 2, 1, 256))),       # n1 = 2: clusters of two pairs, A multicast
+    (2, ((16, 1, 1, 128), (16, 32), (8, 2, 1, 128))),     # n1 = 2 with single-CTA MMAs
 ])
 def test_umma_tail_split(fam, cfg, monkeypatch):
     # DESIGN.md §6 tail split: tiles % co-resident clusters != 0, so the last tiles' k-blocks are
@@ -336,6 +339,8 @@ def test_tn_layout_perceptron(fam):
     sp = Spec(m, k, n, family=fam)
     cfgs = [s for s in space.enumerate_configs(sp) if space.legitimate(sp, s)]
     pick = [cfgs[i] for i in SplitMix64(5).sample_indices(len(cfgs), 12)]
+    if fam != tt.FAM_F32_SIMT:                         # A multicast (n1 = 2) with MN-major A boxes
+        pick += [c for c in cfgs if c[2][1] == 2][:3]
     Wd, Xd = to_dev(W, bf16), to_dev(X, bf16)
     for s in pick:
         C = torch.full((m, n), float("nan"), device=DEV)
