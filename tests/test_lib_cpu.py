@@ -260,6 +260,14 @@ def test_binding_simt_and_umma():
     with pytest.raises(tt.TileTuneError) as e:
         tt.binding(ls, space.initial_state(Spec(4096, 4096, 4096)))
     assert e.value.status == tt.E_INFEASIBLE
+    # n1 = 2: clusters of m1 n1 CTAs along N sharing A (multicast); the cluster tile spans n1 n2 n3
+    b = tt.binding(ls, ((16, 2, 1, 128), (32, 128), (8, 2, 1, 256)))
+    assert (b.cluster_x, b.tile_m, b.tile_n) == (4, 256, 512) and b.grid_x % 4 == 0
+    b = tt.binding(ls, ((32, 1, 1, 128), (32, 128), (16, 2, 1, 128)))
+    assert (b.cluster_x, b.tile_m, b.tile_n) == (2, 128, 256) and b.grid_x % 2 == 0
+    with pytest.raises(tt.TileTuneError) as e:                 # n1 = 4 stays outside J_hw
+        tt.binding(ls, ((16, 2, 1, 128), (32, 128), (4, 4, 1, 256)))
+    assert e.value.status == tt.E_INFEASIBLE
 
 
 @pytest.mark.parametrize("width,fam,dims", [(1, 0, (64, 64, 64)), (8, 0, (64, 64, 64)), (4, 1, (512, 512, 512))])

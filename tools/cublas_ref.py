@@ -27,7 +27,8 @@ def timed(fn, steps=30, warmup=5):
 
 def main():
     out = []
-    for name, n, dt, tf32 in [("f32", 2048, torch.float32, False), ("f32", 4096, torch.float32, False),
+    for name, n, dt, tf32 in [("f32", 1024, torch.float32, False), ("f32", 2048, torch.float32, False),
+                              ("f32", 4096, torch.float32, False),
                               ("tf32", 2048, torch.float32, True), ("tf32", 4096, torch.float32, True),
                               ("bf16", 1024, torch.bfloat16, False), ("bf16", 2048, torch.bfloat16, False),
                               ("bf16", 4096, torch.bfloat16, False), ("bf16", 8192, torch.bfloat16, False)]:
