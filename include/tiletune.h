@@ -50,6 +50,9 @@ typedef enum {
   TT_FAM_TF32_UMMA = 2,    /* K2: tcgen05.mma kind::tf32, fp32 storage, fp32 accumulate */
   TT_FAM_BF16_UMMA = 3     /* K3: tcgen05.mma kind::f16 with bf16 A/B, fp32 accumulate */
 } tt_family;
+/* UMMA level map (reading Z2): m = [cluster tiles, cta_group 1|2, M atoms per CTA 1|2, 128],
+ * n = [cluster tiles, pairs per cluster along N 1|2 (2 = A shared by TMA multicast), N atoms per
+ * CTA 1|2, UMMA_N], k = [trips, BK].  SIMT: m / n = [CTAs, thread groups, lanes, register tile]. */
 
 /* Storage of A.  NN: A row-major [M][K] (the plain definition, reading Z14).  TN: the paper's
  * perceptron workload Y = W^T X with W in R^(k x m): the caller passes W row-major
@@ -165,7 +168,7 @@ typedef struct {
   int32_t family;
   int64_t grid_x, grid_y, grid_z;
   int32_t block_x;
-  int32_t cluster_x;
+  int32_t cluster_x;       /* CTAs per cluster (UMMA: cta_group x n1) */
   int32_t smem_bytes;      /* dynamic shared memory */
   int32_t stages;          /* pipeline depth */
   int32_t tile_m, tile_n, tile_k;   /* per-cluster output tile and K step */
