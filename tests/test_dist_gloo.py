@@ -20,7 +20,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, algo, out):
+def _worker(rank, world, port, algo, out, dynamic=False):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -36,7 +36,8 @@ def _worker(rank, world, port, algo, out):
         measured.append(s)
         return costs.t2_cost(sp, s)
 
-    ev = tdist.ShardedEvaluator(measure_one)
+    ev = tdist.ShardedEvaluator(measure_one, store=tdist.default_store() if dynamic else None)
+    assert (ev.store is not None) == dynamic
     if algo == "gbfs":
         res = tt.gbfs_search(64, 64, 64, 300, tt.search_opts(seed=4, width=8), batch=ev)
     else:
@@ -46,12 +47,12 @@ def _worker(rank, world, port, algo, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("algo", ["gbfs", "na2c"])
-def test_sharded_search_matches_oracle(algo):
+@pytest.mark.parametrize("algo,dynamic", [("gbfs", False), ("na2c", False), ("gbfs", True), ("na2c", True)])
+def test_sharded_search_matches_oracle(algo, dynamic):
     world = 2
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), algo, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), algo, out, dynamic), nprocs=world, join=True)
     sp = Spec(64, 64, 64)
     tab = costs.table(sp, lambda s: costs.t2_cost(sp, s))
     if algo == "gbfs":
@@ -63,7 +64,8 @@ def test_sharded_search_matches_oracle(algo):
     t1, n1, rounds1, rr1 = out[1]
     assert t0 == t1 == ref                                 # identical traversal on every rank = oracle
     assert n0 + n1 == len(ref)                             # each candidate measured exactly once
-    assert abs(n0 - n1) <= rounds0                         # round-robin balance
+    if not dynamic:
+        assert abs(n0 - n1) <= rounds0                     # round-robin balance
     assert rr0 == (0, 4096) and rr1 == (4096, 8192)        # exact row partition
 
 def test_projection():
@@ -72,3 +74,6 @@ def test_projection():
     # G = 2: round 2 shares (1+3, 2+4) -> 6; round 3 -> 2.0
     assert tdist.projected_sharded_wall(rt, 2) == 1.0 + 6.0 + 2.0
     assert tdist.projected_sharded_wall(rt, 8, per_round_s=0.1) == 1.1 + 4.1 + 0.6
+    # dynamic: list scheduling in index order, each candidate to the first free rank
+    assert tdist.projected_sharded_wall([[4.0, 1.0, 1.0, 1.0, 1.0]], 2, dynamic=True) == 4.0
+    assert tdist.projected_sharded_wall([[4.0, 1.0, 1.0, 1.0, 1.0]], 2) == 6.0
