@@ -43,6 +43,8 @@ WORKLOADS = {
     "bf16_4096": (4096, 4096, 4096, 3, 128),
     # BASELINE configs[4]: 8192^3 row-partitioned; M per rank = 8192 / N GPUs (strong scaling)
     "bf16_8192": (8192, 8192, 8192, 3, 128),
+    # one rank's shard of bf16_8192 at N = 8 (per-shard config tuned on (1024, 8192, 8192))
+    "bf16_8192_shard8": (1024, 8192, 8192, 3, 128),
     "tf32_2048": (2048, 2048, 2048, 2, 128),
     "tf32_4096": (4096, 4096, 4096, 2, 128),
     # fp32 SIMT: 0.1 % of the raw space (the paper's budget, P:375 / P:397), s0 untiled
