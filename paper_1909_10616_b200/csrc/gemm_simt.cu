@@ -18,6 +18,8 @@
 // multiples of 4 and results are stored with STG.128.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "device.hpp"
 
 namespace tt {
@@ -102,13 +104,16 @@ __device__ __forceinline__ void fma_frag(const float* a, const float* b, float (
   }
 }
 
-template <int TM, int TN>
+// BKF > 0: the K slab is a compile-time constant, so the k-step loop unrolls completely and the
+// compiler hoists the shared-memory fragment loads as far ahead as registers allow (small register
+// tiles otherwise expose the LDS latency).  BKF = 0: the generic instance.
+template <int TM, int TN, int BKF = 0>
 __global__ void __launch_bounds__(MaxThreads<TM * TN>::value)
 k1_simt(SimtArgs p) {
   extern __shared__ __align__(16) float smem[];
   const int BM = p.m1 * p.m2 * TM;
   const int BN = p.n1 * p.n2 * TN;
-  const int BK = p.bk;
+  const int BK = BKF > 0 ? BKF : p.bk;
   const int LDA = BM + 4, LDB = BN + 4;
   const int NS = p.stages;               // 2 or 3 smem slots (binder: 3 when occupancy allows)
   float* Bs = smem;                      // [NS][BK][LDB]
@@ -216,6 +221,7 @@ k1_simt(SimtArgs p) {
     float a0[TM], b0[TN], a1[TM], b1[TN];
     load_frag<TM, TN, kVecA>(as, bs, 0, LDA, LDB, a0, b0);
     int kk = 0;
+#pragma unroll(BKF > 0 ? BKF / 2 : 1)
     for (; kk + 2 <= BK; kk += 2) {
       load_frag<TM, TN, kVecA>(as, bs, kk + 1, LDA, LDB, a1, b1);
       fma_frag<TM, TN, kPair>(a0, b0, acc, acc2);
@@ -268,6 +274,20 @@ template <int... LMs>
 constexpr void fill_all(KernelFn (&t)[7][7], std::integer_sequence<int, LMs...>) {
   (fill_row<LMs>(t, std::make_integer_sequence<int, 7>{}), ...);
 }
+
+// Fixed-slab instances (register tile, BK) for the small register tiles the searches pick at the
+// paper's 512^3 / 1024^3 shapes (measured +9 % / +27 %, profiles/r3_epilogue.md); a config
+// matching one exactly runs it, everything else the generic instance.
+struct FixedInst {
+  int tm, tn, bk;
+  KernelFn fn;
+};
+#define TT_FIXED3(TM, TN) {TM, TN, 32, &k1_simt<TM, TN, 32>}, {TM, TN, 64, &k1_simt<TM, TN, 64>}, \
+                          {TM, TN, 128, &k1_simt<TM, TN, 128>}
+// register tiles of <= 32 accumulators (larger ones spill at their launch bound when fully
+// unrolled, and already cover the LDS latency with the generic loop)
+const FixedInst kFixed[] = {TT_FIXED3(4, 4), TT_FIXED3(4, 8), TT_FIXED3(8, 4)};
+#undef TT_FIXED3
 
 struct Table {
   KernelFn fn[7][7] = {};
@@ -330,6 +350,27 @@ tt_status simt_launch(const Space& sp, const State& s, const float* A, const flo
                  err, "cudaFuncSetAttribute(k1_simt)"))
       return TT_E_CUDA;
     tb.attr_set[lm][ln] = true;
+  }
+  // TT_SIMT_FIXED=0 (experiments) keeps the generic instance for every config
+  static const bool use_fixed = [] {
+    const char* e = std::getenv("TT_SIMT_FIXED");
+    return !(e && e[0] == '0');
+  }();
+  if (use_fixed) {
+    static bool fixed_attr[sizeof(kFixed) / sizeof(kFixed[0])] = {};
+    for (size_t i = 0; i < sizeof(kFixed) / sizeof(kFixed[0]); ++i) {
+      const FixedInst& f = kFixed[i];
+      if (f.tm == li.reg_tile_m && f.tn == li.reg_tile_n && f.bk == li.tile_k) {
+        if (!fixed_attr[i]) {
+          if (!cuda_ok(cudaFuncSetAttribute((const void*)f.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            kSmemPerCta), err, "cudaFuncSetAttribute(k1_simt fixed)"))
+            return TT_E_CUDA;
+          fixed_attr[i] = true;
+        }
+        fn = f.fn;
+        break;
+      }
+    }
   }
   SimtArgs a;
   a.A = A;

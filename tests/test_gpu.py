@@ -83,6 +83,21 @@ def test_simt_random_configs_bit_exact(dims, n):
         assert og.normwise_error(C, R) <= 1e-4
 
 
+def test_simt_fixed_slab_instances_bit_exact():
+    # register tiles of <= 32 accumulators with BK in {32, 64, 128} run compile-time-BK instances
+    # (gemm_simt.cu kFixed): same fmaf chain, so still bit-identical to the sequential oracle
+    m, k, n = 512, 256, 384
+    sp = Spec(m, k, n, family=hw.FAM_F32_SIMT)
+    A, B = host_inputs(m, n, k)
+    ref32 = og.gemm_fmaf(A, B)
+    picked = [s for s in (c for c in space.enumerate_configs(sp) if space.legitimate(sp, c))
+              if s[1][1] in (32, 64, 128) and (s[0][3], s[2][3]) in ((4, 4), (4, 8), (8, 4))]
+    pick = [picked[i] for i in SplitMix64(11).sample_indices(len(picked), 24)]
+    assert {s[1][1] for s in pick} == {32, 64, 128}
+    for s in pick:
+        assert np.array_equal(run(tt.FAM_F32_SIMT, s, A, B), ref32), s
+
+
 def test_simt_s0_identity_ones_degenerate():
     B = synth.uniform_f32(2, 128, 96)
     I = np.eye(128, dtype=np.float32)

@@ -4,5 +4,5 @@
 # G-BFS vs N-A2C vs random search.
 OUT=gpurun_out
 timeout 3000 python -m paper_1909_10616_b200.cli compare --m 1024 --k 1024 --n 1024 --family f32 --max-evals 900 \
-    --seeds 0-9 --repeats 5 --out $OUT/cmp_f32_1024 > $OUT/cmp_f32_1024.log 2>&1
+    --seeds 0-9 --repeats 5 --shared-cache --out $OUT/cmp_f32_1024 > $OUT/cmp_f32_1024.log 2>&1
 tail -40 $OUT/cmp_f32_1024.log
