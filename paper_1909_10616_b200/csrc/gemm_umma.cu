@@ -878,12 +878,7 @@ void plan_of(const Space& sp, const State& s, Plan* pl) {
   a.stage_bytes = (int)umma_stage_bytes(fam, s);
   a.tx_bytes = (uint32_t)(a.a_stage_bytes + a.n2 * a.nb * a.bk * elem);
   a.stages = std::min<int>(kUmmaMaxStages, kUmmaPipeSmem / a.stage_bytes);
-  // TT_UMMA_STAGES (experiments): fewer pipeline stages; the freed shared memory goes to the
-  // epilogue staging.  Leftover pipeline memory always does.
-  if (const char* e = std::getenv("TT_UMMA_STAGES")) {
-    const int want = std::atoi(e);
-    if (want >= 2 && want < a.stages) a.stages = want;
-  }
+  // leftover pipeline shared memory goes to the epilogue staging
   {
     const int spare = kUmmaPipeSmem - a.stages * a.stage_bytes;
     a.epi_bufs = std::min(kEpiMaxBufs, kEpiBytes / (kEpiWarps * kEpiBoxBytes) + std::max(0, spare) / (kEpiWarps * kEpiBoxBytes));
