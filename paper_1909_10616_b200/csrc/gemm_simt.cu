@@ -107,8 +107,8 @@ __device__ __forceinline__ void fma_frag(const float* a, const float* b, float (
 // BKF > 0: the K slab is a compile-time constant, so the k-step loop unrolls completely and the
 // compiler hoists the shared-memory fragment loads as far ahead as registers allow (small register
 // tiles otherwise expose the LDS latency).  BKF = 0: the generic instance.
-template <int TM, int TN, int BKF = 0>
-__global__ void __launch_bounds__(MaxThreads<TM * TN>::value)
+template <int TM, int TN, int BKF = 0, int LB = MaxThreads<TM * TN>::value>
+__global__ void __launch_bounds__(LB)
 k1_simt(SimtArgs p) {
   extern __shared__ __align__(16) float smem[];
   const int BM = p.m1 * p.m2 * TM;
@@ -279,13 +279,17 @@ constexpr void fill_all(KernelFn (&t)[7][7], std::integer_sequence<int, LMs...>)
 // paper's 512^3 / 1024^3 shapes (measured +9 % / +27 %, profiles/r3_epilogue.md); a config
 // matching one exactly runs it, everything else the generic instance.
 struct FixedInst {
-  int tm, tn, bk;
+  int tm, tn, bk, lb;   // lb: the instance's launch bound (configs with more threads use others)
   KernelFn fn;
 };
-#define TT_FIXED3(TM, TN) {TM, TN, 32, &k1_simt<TM, TN, 32>}, {TM, TN, 64, &k1_simt<TM, TN, 64>}, \
-                          {TM, TN, 128, &k1_simt<TM, TN, 128>}
+#define TT_FIXED3(TM, TN)                                                                   \
+  {TM, TN, 32, MaxThreads<TM * TN>::value, &k1_simt<TM, TN, 32>},                            \
+      {TM, TN, 64, MaxThreads<TM * TN>::value, &k1_simt<TM, TN, 64>},                        \
+      {TM, TN, 128, MaxThreads<TM * TN>::value, &k1_simt<TM, TN, 128>}
 // register tiles of <= 32 accumulators (larger ones spill at their launch bound when fully
 // unrolled, and already cover the LDS latency with the generic loop)
+// (8 x 8 tiles with BK 16/32 at launch bound 128/256 measured +8 % for 8 x 8 configs but left
+// the best-found 2048^3 / 4096^3 results, which use 16 x 8 tiles, unchanged: not kept)
 const FixedInst kFixed[] = {TT_FIXED3(4, 4), TT_FIXED3(4, 8), TT_FIXED3(8, 4)};
 #undef TT_FIXED3
 
@@ -360,7 +364,7 @@ tt_status simt_launch(const Space& sp, const State& s, const float* A, const flo
     static bool fixed_attr[sizeof(kFixed) / sizeof(kFixed[0])] = {};
     for (size_t i = 0; i < sizeof(kFixed) / sizeof(kFixed[0]); ++i) {
       const FixedInst& f = kFixed[i];
-      if (f.tm == li.reg_tile_m && f.tn == li.reg_tile_n && f.bk == li.tile_k) {
+      if (f.tm == li.reg_tile_m && f.tn == li.reg_tile_n && f.bk == li.tile_k && li.block_x <= f.lb) {
         if (!fixed_attr[i]) {
           if (!cuda_ok(cudaFuncSetAttribute((const void*)f.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             kSmemPerCta), err, "cudaFuncSetAttribute(k1_simt fixed)"))
