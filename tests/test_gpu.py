@@ -16,7 +16,7 @@ if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import synth  # noqa: E402
-from oracle import costs, gbfs as ogbfs, gemm as og, hw, space  # noqa: E402
+from oracle import na2c as ona2c, costs, gbfs as ogbfs, gemm as og, hw, space  # noqa: E402
 from oracle.rng import SplitMix64  # noqa: E402
 from oracle.space import Spec  # noqa: E402
 from paper_1909_10616_b200 import tiletune as tt  # noqa: E402
@@ -315,12 +315,19 @@ def test_gbfs_device_search_replay_parity():
 
 
 def test_na2c_device_search():
+    # live N-A2C (eps = 0.8: policy sampled, networks trained every batch) on the SIMT space of
+    # 512^3; replaying its (state -> cost) table through the oracle's Algorithm 2 reproduces the
+    # identical sequence of evaluated states (reading Z24 makes the network arithmetic exact)
     ctx = tt.Context(0)
     res = tt.na2c_search(512, 512, 512, 64, tt.search_opts(family=1, seed=1), ctx=ctx)
     ctx.close()
     assert res.evals == 64 and res.best_cost < res.trace[0]["cost"]
     states = [r["state"] for r in res.trace]
     assert len(set(states)) == 64
+    table = {r["state"]: r["cost"] for r in res.trace}
+    sp = Spec(512, 512, 512, family=1)
+    o = ona2c.na2c(sp, lambda batch: [table[s] for s in batch], budget=64, params=ona2c.Params(), seed=1)
+    assert [r.state for r in o.trace] == states
 
 
 def test_bf16_exhaustive_vs_gbfs_4096():
