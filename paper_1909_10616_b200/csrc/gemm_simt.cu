@@ -53,10 +53,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-template <int ACC>
-struct MaxThreads {
-  static constexpr int value = ACC <= 16 ? 1024 : (ACC <= 64 ? 512 : 256);
-};
+constexpr int max_threads(int acc) { return acc <= 16 ? 1024 : (acc <= 64 ? 512 : 256); }
 
 template <int TM, int TN, bool VECA>
 __device__ __forceinline__ void load_frag(const float* as, const float* bs, int kk, int LDA, int LDB, float* a,
@@ -107,7 +104,7 @@ __device__ __forceinline__ void fma_frag(const float* a, const float* b, float (
 // BKF > 0: the K slab is a compile-time constant, so the k-step loop unrolls completely and the
 // compiler hoists the shared-memory fragment loads as far ahead as registers allow (small register
 // tiles otherwise expose the LDS latency).  BKF = 0: the generic instance.
-template <int TM, int TN, int BKF = 0, int LB = MaxThreads<TM * TN>::value>
+template <int TM, int TN, int BKF = 0, int LB = max_threads(TM * TN)>
 __global__ void __launch_bounds__(LB)
 k1_simt(SimtArgs p) {
   extern __shared__ __align__(16) float smem[];
@@ -283,9 +280,9 @@ struct FixedInst {
   KernelFn fn;
 };
 #define TT_FIXED3(TM, TN)                                                                   \
-  {TM, TN, 32, MaxThreads<TM * TN>::value, &k1_simt<TM, TN, 32>},                            \
-      {TM, TN, 64, MaxThreads<TM * TN>::value, &k1_simt<TM, TN, 64>},                        \
-      {TM, TN, 128, MaxThreads<TM * TN>::value, &k1_simt<TM, TN, 128>}
+  {TM, TN, 32, max_threads(TM * TN), &k1_simt<TM, TN, 32>},                            \
+      {TM, TN, 64, max_threads(TM * TN), &k1_simt<TM, TN, 64>},                        \
+      {TM, TN, 128, max_threads(TM * TN), &k1_simt<TM, TN, 128>}
 // register tiles of <= 32 accumulators (larger ones spill at their launch bound when fully
 // unrolled, and already cover the LDS latency with the generic loop)
 // (8 x 8 tiles with BK 16/32 at launch bound 128/256 measured +8 % for 8 x 8 configs but left

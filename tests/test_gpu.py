@@ -294,9 +294,17 @@ def test_gemm_host_matches_device():
     A, B = host_inputs(M, N, K)
     Ah, Bh = torch.from_numpy(A).pin_memory(), torch.from_numpy(B).pin_memory()
     Ch = torch.empty(M, N).pin_memory()
-    s = ((2, 2, 8, 8), (64, 8), (2, 4, 4, 8))
+    s = ((2, 2, 8, 8), (64, 8), (2, 4, 4, 8))      # 2 x 2 blocks of the host pipeline
     ctx.gemm_host(Ah, Bh, Ch, 1, s)
     assert np.array_equal(Ch.numpy(), og.gemm_fmaf(A, B))
+    # bf16 tcgen05 through the 2-D block pipeline (4 x 2 blocks, packed B column chunks)
+    M, N, K = 1024, 1024, 512
+    A, B = host_inputs(M, N, K, bf16=True)
+    Ah = torch.from_numpy(synth.to_bf16_bits(A).view(np.int16)).view(torch.bfloat16).pin_memory()
+    Bh = torch.from_numpy(synth.to_bf16_bits(B).view(np.int16)).view(torch.bfloat16).pin_memory()
+    Ch = torch.full((M, N), float("nan")).pin_memory()
+    ctx.gemm_host(Ah, Bh, Ch, 3, ((4, 2, 1, 128), (8, 64), (4, 1, 1, 256)))
+    assert og.normwise_error(Ch.numpy(), og.gemm_f64(A, B)) <= 5e-3
     ctx.close()
 
 
