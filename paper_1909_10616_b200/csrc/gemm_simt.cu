@@ -419,11 +419,12 @@ int simt_per_sm(KernelFn fn, int threads, int smem) {
   return n;
 }
 
-// Tail re-tiling: TT_SIMT_TAIL = 0 off, 2 forced wherever the tile count leaves a
-// partial wave (tests), unset / 1 = the measured policy.  Read per launch.
+// Tail re-tiling: TT_SIMT_TAIL = 0 off, 1 the measured policy, 2 forced wherever
+// the tile count leaves a partial wave (tests); unset = kSimtTailDefault.  Read per launch.
+constexpr int kSimtTailDefault = 0;
 int simt_tail_mode() {
   const char* e = std::getenv("TT_SIMT_TAIL");
-  if (!e || !e[0]) return 1;
+  if (!e || !e[0]) return kSimtTailDefault;
   return e[0] == '0' ? 0 : (e[0] == '2' ? 2 : 1);
 }
 
