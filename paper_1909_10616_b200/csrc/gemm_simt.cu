@@ -19,10 +19,6 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
-#include <string>
-#include <tuple>
-#include <mutex>
-#include <map>
 
 #include "device.hpp"
 
@@ -43,12 +39,6 @@ struct SimtArgs {
   int a_vec16;  // TN: 16-byte cp.async of W rows legal
   int c_vec;    // C rows 16-byte aligned (STG.128 legal)
   int b_vec;  // B rows 16-byte aligned (16-byte cp.async legal)
-  // 1-D grid over tiles (row-major over (m0, n0)): CTA b covers tile tile0 + b / split, row part
-  // b % split of it (split = 2: the tail re-tiling of DESIGN.md §6 runs half-height CTAs)
-  int n_tiles_x;   // n0
-  int tile0;
-  int split;       // 1, or 2 (this launch's CTA tile is the upper / lower half of the config tile)
-  int bm_full;     // rows of the config tile (BM for split = 1)
 };
 
 __device__ __forceinline__ void cp_async4(float* dst, const float* src) {
@@ -136,13 +126,9 @@ k1_simt(SimtArgs p) {
   const int col0 = gn * (p.n2 * TN) + ln * TN;
 
   const int64_t K = p.K, N = p.N;
-  const int tile = p.tile0 + (int)blockIdx.x / p.split;
-  const int part = (int)blockIdx.x - ((int)blockIdx.x / p.split) * p.split;
-  const int by = tile / p.n_tiles_x, bx = tile - (tile / p.n_tiles_x) * p.n_tiles_x;
-  const int64_t cta_row = (int64_t)by * p.bm_full + (int64_t)part * BM;
-  const float* Ab = p.a_tn ? p.A + cta_row : p.A + cta_row * K;
+  const float* Ab = p.a_tn ? p.A + (int64_t)blockIdx.y * BM : p.A + (int64_t)blockIdx.y * BM * K;
   const int64_t M = p.M;
-  const float* Bb = p.B + (int64_t)bx * BN;
+  const float* Bb = p.B + (int64_t)blockIdx.x * BN;
 
   auto load = [&](int kt, int buf) {
     float* as = As + buf * BK * LDA;
@@ -253,7 +239,7 @@ k1_simt(SimtArgs p) {
       }
   }
 
-  float* Cb = p.C + (cta_row + row0) * N + (int64_t)bx * BN + col0;
+  float* Cb = p.C + ((int64_t)blockIdx.y * BM + row0) * N + (int64_t)blockIdx.x * BN + col0;
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
     if constexpr (TN % 4 == 0) {
@@ -349,21 +335,21 @@ tt_status simt_bind(const Space& sp, const State& s, tt_launch_info* info, std::
   return TT_OK;
 }
 
-namespace {
-
-// generic instance of the register tile, or the compile-time-BK one when it matches
-KernelFn pick_kernel(int tm, int tn, int bk, int threads, std::string* err) {
-  const int lm = ilog2(tm), ln = ilog2(tn);
+tt_status simt_launch(const Space& sp, const State& s, const float* A, const float* B, float* C,
+                      cudaStream_t stream, std::string* err) {
+  tt_launch_info li;
+  simt_bind(sp, s, &li, err);
+  const int lm = ilog2(li.reg_tile_m), ln = ilog2(li.reg_tile_n);
   Table& tb = table();
-  KernelFn fn = (lm < 7 && ln < 7) ? tb.fn[lm][ln] : nullptr;
+  KernelFn fn = tb.fn[lm][ln];
   if (!fn) {
     *err = "no SIMT kernel instance for this register tile";
-    return nullptr;
+    return TT_E_UNSUPPORTED;
   }
   if (!tb.attr_set[lm][ln]) {
     if (!cuda_ok(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemPerCta),
                  err, "cudaFuncSetAttribute(k1_simt)"))
-      return nullptr;
+      return TT_E_CUDA;
     tb.attr_set[lm][ln] = true;
   }
   // TT_SIMT_FIXED=0 (experiments) keeps the generic instance for every config
@@ -375,67 +361,18 @@ KernelFn pick_kernel(int tm, int tn, int bk, int threads, std::string* err) {
     static bool fixed_attr[sizeof(kFixed) / sizeof(kFixed[0])] = {};
     for (size_t i = 0; i < sizeof(kFixed) / sizeof(kFixed[0]); ++i) {
       const FixedInst& f = kFixed[i];
-      if (f.tm == tm && f.tn == tn && f.bk == bk && threads <= f.lb) {
+      if (f.tm == li.reg_tile_m && f.tn == li.reg_tile_n && f.bk == li.tile_k && li.block_x <= f.lb) {
         if (!fixed_attr[i]) {
           if (!cuda_ok(cudaFuncSetAttribute((const void*)f.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             kSmemPerCta), err, "cudaFuncSetAttribute(k1_simt fixed)"))
-            return nullptr;
+            return TT_E_CUDA;
           fixed_attr[i] = true;
         }
-        return f.fn;
+        fn = f.fn;
+        break;
       }
     }
   }
-  return fn;
-}
-
-int simt_num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
-
-// co-resident CTAs per SM of an instance at this block size and smem (cached)
-int simt_per_sm(KernelFn fn, int threads, int smem) {
-  static std::mutex mu;
-  static std::map<std::tuple<const void*, int, int, int>, int> cache;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(mu);
-  const auto key = std::make_tuple((const void*)fn, threads, smem, dev);
-  auto it = cache.find(key);
-  if (it != cache.end()) return it->second;
-  int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, (size_t)smem) != cudaSuccess) {
-    cudaGetLastError();
-    n = 0;
-  }
-  cache[key] = n;
-  return n;
-}
-
-// Tail re-tiling: TT_SIMT_TAIL = 0 off, 1 the measured policy, 2 forced wherever
-// the tile count leaves a partial wave (tests); unset = kSimtTailDefault.  Read per launch.
-constexpr int kSimtTailDefault = 0;
-int simt_tail_mode() {
-  const char* e = std::getenv("TT_SIMT_TAIL");
-  if (!e || !e[0]) return kSimtTailDefault;
-  return e[0] == '0' ? 0 : (e[0] == '2' ? 2 : 1);
-}
-
-}  // namespace
-
-tt_status simt_launch(const Space& sp, const State& s, const float* A, const float* B, float* C,
-                      cudaStream_t stream, std::string* err) {
-  tt_launch_info li;
-  simt_bind(sp, s, &li, err);
-  KernelFn fn = pick_kernel(li.reg_tile_m, li.reg_tile_n, li.tile_k, li.block_x, err);
-  if (!fn) return err->find("instance") != std::string::npos ? TT_E_UNSUPPORTED : TT_E_CUDA;
   SimtArgs a;
   a.A = A;
   a.B = B;
@@ -449,6 +386,8 @@ tt_status simt_launch(const Space& sp, const State& s, const float* A, const flo
   a.n2 = (int)s.f[2][2];
   a.bk = (int)s.f[1][1];
   a.k0 = (int)s.f[1][0];
+  const int64_t LDB = li.tile_n + 4;
+  (void)LDB;
   auto lg = [](int64_t v) -> int { if (v <= 0 || (v & (v - 1))) return -1; int l = 0; while ((int64_t(1) << l) < v) ++l; return l; };
   a.bk_sh = lg(a.bk);
   a.bq_sh = (li.tile_n % 4 == 0) ? lg(li.tile_n / 4) : -1;
@@ -456,46 +395,11 @@ tt_status simt_launch(const Space& sp, const State& s, const float* A, const flo
   a.a_tn = sp.layout == TT_LAYOUT_TN ? 1 : 0;
   a.c_vec = (a.N % 4 == 0 && ((uintptr_t)C % 16) == 0) ? 1 : 0;
   a.stages = li.stages;
-  auto vec16 = [&](int64_t tile_m) {
-    return (tile_m % 4 == 0 && a.M % 4 == 0 && ((uintptr_t)A % 16) == 0 &&
-            ((2 * (int64_t)a.bk * (li.tile_n + 4)) % 4) == 0) ? 1 : 0;
-  };
-  a.a_vec16 = vec16(li.tile_m);
-  a.n_tiles_x = (int)li.grid_x;
-  a.tile0 = 0;
-  a.split = 1;
-  a.bm_full = li.tile_m;
-  const int64_t T = li.grid_x * li.grid_y;
-
-  // Tail re-tiling: when the tiles leave a partial last wave on the co-resident CTA slots S, the
-  // last T mod S tiles run as twice as many half-height CTAs (register tile m3 / 2, same threads)
-  // in a second launch.  Every output is still one fmaf chain in k order, so results are
-  // bit-identical.  Policy (measured): a tail of at most 60 % of a wave behind at
-  // least one full wave.
-  int64_t r = 0;
-  const int mode = simt_tail_mode();
-  if (mode != 0 && li.reg_tile_m >= 2) {
-    const int64_t S = (int64_t)simt_per_sm(fn, li.block_x, li.smem_bytes) * simt_num_sms();
-    if (S > 0 && T % S != 0) {
-      if (mode == 2) r = T > S ? T % S : T;
-      else if (T > S && (T % S) * 10 <= S * 6) r = T % S;
-    }
-  }
-  if (T - r > 0) {
-    fn<<<(unsigned)(T - r), li.block_x, li.smem_bytes, stream>>>(a);
-    if (!cuda_ok(cudaGetLastError(), err, "k1_simt launch")) return TT_E_CUDA;
-  }
-  if (r > 0) {
-    KernelFn fn2 = pick_kernel(li.reg_tile_m / 2, li.reg_tile_n, li.tile_k, li.block_x, err);
-    if (!fn2) return TT_E_CUDA;
-    SimtArgs a2 = a;
-    a2.tile0 = (int)(T - r);
-    a2.split = 2;
-    a2.a_vec16 = vec16(li.tile_m / 2);
-    const int64_t slot = (li.tile_m / 2 + li.tile_n + 2 * kSimtPad) * li.tile_k * 4;
-    fn2<<<(unsigned)(2 * r), li.block_x, (size_t)(li.stages * slot), stream>>>(a2);
-    if (!cuda_ok(cudaGetLastError(), err, "k1_simt tail launch")) return TT_E_CUDA;
-  }
+  a.a_vec16 = (li.tile_m % 4 == 0 && a.M % 4 == 0 && ((uintptr_t)A % 16) == 0 &&
+               ((2 * (int64_t)a.bk * (li.tile_n + 4)) % 4) == 0) ? 1 : 0;
+  dim3 grid((unsigned)li.grid_x, (unsigned)li.grid_y, 1);
+  fn<<<grid, li.block_x, li.smem_bytes, stream>>>(a);
+  if (!cuda_ok(cudaGetLastError(), err, "k1_simt launch")) return TT_E_CUDA;
   return TT_OK;
 }
 

@@ -98,21 +98,6 @@ def test_simt_fixed_slab_instances_bit_exact():
         assert np.array_equal(run(tt.FAM_F32_SIMT, s, A, B), ref32), s
 
 
-@pytest.mark.parametrize("dims", [(512, 512, 512), (1024, 256, 768)])
-def test_simt_tail_retiling_bit_exact(dims, monkeypatch):
-    # DESIGN.md §6 tail re-tiling, forced (TT_SIMT_TAIL=2): the last tiles run as half-height CTAs
-    # in a second launch; every output is still the sequential fmaf chain
-    monkeypatch.setenv("TT_SIMT_TAIL", "2")
-    m, k, n = dims
-    sp = Spec(m, k, n, family=hw.FAM_F32_SIMT)
-    A, B = host_inputs(m, n, k)
-    ref32 = og.gemm_fmaf(A, B)
-    cfgs = [c for c in _random_feasible(sp, 40, seed=m + n) if c[0][3] >= 2][:16]
-    assert cfgs
-    for s in cfgs:
-        assert np.array_equal(run(tt.FAM_F32_SIMT, s, A, B), ref32), s
-
-
 def test_simt_s0_identity_ones_degenerate():
     B = synth.uniform_f32(2, 128, 96)
     I = np.eye(128, dtype=np.float32)
