@@ -6,7 +6,8 @@ sys.path.insert(0, '.')
 import torch
 from paper_1909_10616_b200 import tiletune as tt
 dev = torch.device('cuda:0')
-for fam, n, cfgs in [(1, 128, [((2, 2, 8, 4), (16, 8), (2, 2, 4, 8)), ((128, 1, 1, 1), (128, 1), (128, 1, 1, 1)), ((1, 4, 4, 8), (4, 32), (2, 2, 8, 4))]),
+for fam, n, cfgs in [(1, 128, [((2, 2, 8, 4), (16, 8), (2, 2, 4, 8)), ((128, 1, 1, 1), (128, 1), (128, 1, 1, 1)), ((1, 4, 4, 8), (4, 32), (2, 2, 8, 4)),
+                             ((2, 4, 4, 4), (1, 128), (2, 4, 2, 8)), ((2, 2, 8, 4), (2, 64), (2, 4, 4, 4))]),   # fixed-BK instances
                      (3, 512, [((4, 1, 1, 128), (8, 64), (4, 1, 1, 128)), ((1, 2, 2, 128), (8, 64), (2, 1, 1, 256)), ((2, 2, 1, 128), (32, 16), (16, 1, 1, 32))]),
                      (2, 256, [((2, 1, 1, 128), (8, 32), (2, 1, 1, 128)), ((1, 2, 1, 128), (32, 8), (1, 1, 1, 256))])]:
     dt = torch.bfloat16 if fam == 3 else torch.float32
@@ -32,6 +33,15 @@ for fam, n, cfgs in [(3, 512, [((4, 1, 1, 128), (8, 64), (4, 1, 1, 128)), ((2, 2
         torch.cuda.synchronize()
         ref = A.float() @ B.float()
         print("split", info.split_tiles, fam, s, float((C - ref).abs().max() / ref.abs().max()))
+# A-multicast clusters (n1 = 2), plain and split
+for cfg in [((2, 2, 1, 128), (4, 128), (1, 2, 1, 256)), ((4, 1, 1, 128), (4, 128), (2, 2, 1, 128))]:
+    A = torch.randn(512, 512, device=dev).to(torch.bfloat16)
+    B = torch.randn(512, 512, device=dev).to(torch.bfloat16)
+    C = torch.empty(512, 512, device=dev)
+    tt.gemm(A, B, C, 3, cfg)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float()
+    print("multicast", cfg, float((C - ref).abs().max() / ref.abs().max()))
 del os.environ["TT_TAIL_SPLIT"]
 ctx = tt.Context(0)
 smp = ctx.measure(tt.make_space(512, 512, 512, family=3), ((4, 1, 1, 128), (8, 64), (4, 1, 1, 128)),
