@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define TT_VERSION 4
+#define TT_VERSION 5
 #define TT_MAXD 4  /* maximum loop depth per axis carried in tt_config */
 
 typedef enum {
@@ -161,6 +161,10 @@ typedef struct {
    * T_e = max(steps_T_floor, steps_T - e / steps_T_decay_every) steps; decay_every = 0: constant T. */
   int32_t steps_T_floor, steps_T_decay_every;
   int32_t layout;          /* tt_layout of A for the DEVICE cost source (default NN) */
+  /* Alg. 2 line 24 "Train actor's and critic's neural networks with M" sits inside the
+   * "for s' in B_collect" loop.  1: train after every candidate, in that order;
+   * 0 (default, reading Z18 / S:422): train once after each measured batch. */
+  int32_t train_per_candidate;
 } tt_search_opts;
 
 /* How a config is bound to a launch (a5 of SURVEY §8a; for tests and reports). */
@@ -276,6 +280,15 @@ tt_status tt_ctx_operands(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, int32_t 
  * without J; TT_E_CUDA on a launch error. */
 tt_status tt_measure(tt_ctx* ctx, const tt_space* sp, const tt_config* cfg,
                      const tt_measure_opts* opts, tt_sample* out);
+
+/* The statistic tt_measure reports ("the arithmetic mean for 10 repeated trials"; reading
+ * Z10): from R >= 1 per-repeat mean launch times per_repeat[0..R) (seconds, host array), sets
+ * out->cost_s = median (mean of the two middle values for even R), mean_s = arithmetic mean
+ * (left-to-right sum / R), min_s, stdev_s = sample standard deviation (0 for R = 1) and
+ * repeats = R; the other fields are left untouched.  Pure host function: tt_measure calls exactly
+ * this on its event timings, and it is exported so the statistic can be checked on injected
+ * samples ("fake clock").  TT_E_INVAL for a null pointer or R < 1. */
+tt_status tt_aggregate(const double* per_repeat, int32_t R, tt_sample* out);
 
 /* ---------------------------------------------------------------- searches (B4) */
 

@@ -29,7 +29,8 @@ a guided by the policy").  Readings (Z18):
   * B_collect is truncated to budget - evals, measured as one batch, walked in order.
   * reward r = c_ref / cost(s'), c_ref = cost(initial s0): a positive rescale of Eq. 8's 1/cost.
   * M is a FIFO of capacity ``mem_capacity`` holding every predecessor transition.
-  * training once per batch: ``epochs`` SGD steps, each on ``minibatch`` transitions drawn
+  * training once per batch (``train_per_candidate=True``: after every candidate, Alg. 2's own
+    placement of line 24 inside the line-17 loop): ``epochs`` SGD steps, each on ``minibatch`` transitions drawn
     with replacement via bounded(len(M)) from the network stream.  A = r + gamma V(s') - V(s)
     (V(s') a constant target); critic loss A^2; actor loss -A log pi(a|s) - beta H(pi(.|s)).
   * two SplitMix64 streams: exploration ``seed`` (eps draw, then the action draw), and network
@@ -62,13 +63,17 @@ NN_STREAM_XOR = 0xA2C0A2C0A2C0A2C0
 class Params:
     def __init__(self, steps=3, epsilon=0.8, batch=16, mem_capacity=4096, gamma=0.9, beta=0.01,
                  lr=0.01, clip=1.0, epochs=4, minibatch=64, hidden=64, rollout_cap_factor=50,
-                 max_t_increase=16, steps_floor=1, decay_every=0):
+                 max_t_increase=16, steps_floor=1, decay_every=0, train_per_candidate=False):
         self.steps, self.epsilon, self.batch = steps, epsilon, batch
         self.mem_capacity, self.gamma, self.beta, self.lr, self.clip = mem_capacity, gamma, beta, lr, clip
         self.epochs, self.minibatch, self.hidden = epochs, minibatch, hidden
         self.rollout_cap_factor, self.max_t_increase = rollout_cap_factor, max_t_increase
         # P:336 "the exploration step T can have a decay process": T_e = max(floor, T0 - e // every)
         self.steps_floor, self.decay_every = steps_floor, decay_every
+        # Alg. 2 places "Train actor's and critic's neural networks with M" inside the
+        # "for s' in B_collect" loop: True trains after every candidate, in that order;
+        # False (default, reading Z18 / S:422) trains once after the batch.
+        self.train_per_candidate = train_per_candidate
 
 
 class Agent:
@@ -228,5 +233,8 @@ def na2c(spec: space.Spec,
                 memory.append((pred, acts.index(a), r, s2))
             trace.append(TraceRow(evals, time.perf_counter() - t0, s2, c, best_cost))
             evals += 1
-        agent.train(memory, rng_nn)                                 # line 24 (once per batch)
+            if p.train_per_candidate:
+                agent.train(memory, rng_nn)                         # line 24, inside the loop
+        if not p.train_per_candidate:
+            agent.train(memory, rng_nn)                             # line 24, once per batch (Z18)
     return Result(best_state, best_cost, evals, trace, space.count_configs(spec), None)

@@ -428,6 +428,12 @@ tt_status tt_measure(tt_ctx* ctx, const tt_space* sp, const tt_config* cfg, cons
   return r == TT_OK ? TT_OK : fail(r, err);
 }
 
+tt_status tt_aggregate(const double* per_repeat, int32_t R, tt_sample* out) {
+  if (!per_repeat || !out || R < 1) return fail(TT_E_INVAL, "tt_aggregate needs R >= 1 samples and an output");
+  aggregate_repeats(per_repeat, R, out);
+  return TT_OK;
+}
+
 tt_status tt_gbfs_search(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, uint64_t budget_evals,
                          const tt_search_opts* opts, tt_result* out, tt_trace_row* trace, uint64_t trace_cap) {
   return run_search(gbfs_search, ctx, M, N, K, budget_evals, opts, out, trace, trace_cap);

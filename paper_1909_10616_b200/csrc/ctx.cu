@@ -62,6 +62,26 @@ tt_status launch_gemm(const Space& sp, const State& s, const void* A, const void
   return TT_E_UNSUPPORTED;
 }
 
+// ---------------------------------------------------------------- the cost statistic (Z10)
+// P:369 "the arithmetic mean for 10 repeated trials"; the north star asks for a median: cost =
+// median of the R per-repeat means (mean of the two middle values for even R); mean, min and the
+// sample standard deviation (0 for R = 1) are reported beside it.  Host-only and exported as
+// tt_aggregate, so the exact statistic tt_measure uses is checked against oracle/measure.py.
+void aggregate_repeats(const double* per, int R, tt_sample* out) {
+  std::vector<double> srt(per, per + R);
+  std::sort(srt.begin(), srt.end());
+  double mean = 0;
+  for (int r = 0; r < R; ++r) mean += per[r];
+  mean /= R;
+  double var = 0;
+  for (int r = 0; r < R; ++r) var += (per[r] - mean) * (per[r] - mean);
+  out->cost_s = R % 2 ? srt[R / 2] : 0.5 * (srt[R / 2 - 1] + srt[R / 2]);
+  out->mean_s = mean;
+  out->min_s = srt[0];
+  out->stdev_s = R > 1 ? std::sqrt(var / (R - 1)) : 0.0;
+  out->repeats = R;
+}
+
 // ---------------------------------------------------------------- ctx
 
 Ctx::~Ctx() {
@@ -241,17 +261,7 @@ tt_status Ctx::measure(const Space& sp, const State& s, const tt_measure_opts& m
     cudaEventElapsedTime(&ms, ev[2 + 2 * r], ev[3 + 2 * r]);
     per[r] = ms * 1e-3 / number;
   }
-  std::vector<double> srt = per;
-  std::sort(srt.begin(), srt.end());
-  double mean = 0;
-  for (double x : per) mean += x;
-  mean /= R;
-  double var = 0;
-  for (double x : per) var += (x - mean) * (x - mean);
-  out->cost_s = R % 2 ? srt[R / 2] : 0.5 * (srt[R / 2 - 1] + srt[R / 2]);
-  out->mean_s = mean;
-  out->min_s = srt[0];
-  out->stdev_s = R > 1 ? std::sqrt(var / (R - 1)) : 0.0;
+  aggregate_repeats(per.data(), R, out);
   out->repeats = R;
   out->number = number;
   out->graph_nodes = nodes;

@@ -15,6 +15,9 @@ namespace tt {
 constexpr int kMaxRepeats = 64;
 constexpr int kGraphNodes = 32;   // launches captured per measurement graph
 
+// cost = median of the R per-repeat means; mean / min / stdev beside it (reading Z10, tt_aggregate)
+void aggregate_repeats(const double* per, int R, tt_sample* out);
+
 struct Operands {
   int64_t M = 0, N = 0, K = 0;
   int dtype = 0;  // 0 fp32, 1 bf16

@@ -305,6 +305,58 @@ tt_status na2c_search(const Space& sp, const State& s0, uint64_t budget, const t
   std::vector<double> x(nin), pi;
   std::vector<char> mask;
   std::vector<std::vector<double>> acts, acts2;
+  // Alg. 2 line 24: SGD on minibatches of M (reading Z18)
+  auto train = [&]() {
+    const size_t n = memory.size();
+    if (n > 0) {
+      std::vector<std::vector<double>> gWc, gbc, gWa, gba;
+      for (int ep = 0; ep < epochs; ++ep) {
+        std::vector<size_t> mb(minibatch);
+        for (int b = 0; b < minibatch; ++b) mb[b] = (size_t)rng_nn.bounded(n);
+        critic.zero_like(gWc, gbc);
+        actor.zero_like(gWa, gba);
+        std::vector<double> adv(minibatch);
+        const double B = (double)minibatch;
+        for (int b = 0; b < minibatch; ++b) {
+          const Transition& tr = memory[mb[b]];
+          std::vector<double> xs(nin), x2(nin);
+          sp.features(tr.s, xs.data());
+          sp.features(tr.s2, x2.data());
+          critic.forward(x2.data(), &acts2);
+          const double v2 = acts2.back()[0];
+          critic.forward(xs.data(), &acts);
+          const double v = acts.back()[0];
+          adv[b] = tr.r + o.gamma * v2 - v;
+          const double dv = -2.0 * adv[b] / B;                            // d mean(A^2) / dV(s)
+          critic.backward(acts, &dv, gWc, gbc);
+        }
+        for (int b = 0; b < minibatch; ++b) {
+          const Transition& tr = memory[mb[b]];
+          std::vector<double> xs(nin);
+          sp.features(tr.s, xs.data());
+          actor.forward(xs.data(), &acts);
+          legal_mask(tr.s, &mask);
+          masked_softmax(acts.back(), mask, &pi);
+          double Hs = 0.0;
+          for (int i = 0; i < nact; ++i)
+            if (mask[i] && pi[i] > 0) Hs -= pi[i] * std::log(pi[i]);
+          std::vector<double> dz(nact, 0.0);
+          for (int i = 0; i < nact; ++i) {
+            if (!mask[i]) continue;
+            const double lp = pi[i] > 0 ? std::log(pi[i]) : 0.0;
+            double g = adv[b] * pi[i];                       // -A (onehot - pi), off-action part
+            if (i == tr.a) g -= adv[b];
+            g += o.beta * pi[i] * (lp + Hs);                 // -beta dH/dz
+            dz[i] = g / B;
+          }
+          actor.backward(acts, dz.data(), gWa, gba);
+        }
+        critic.sgd(gWc, gbc, o.lr, o.clip);
+        actor.sgd(gWa, gba, o.lr, o.clip);
+      }
+    }
+  };
+
   tt_status result = TT_OK;
 
   while (evals < budget) {
@@ -386,56 +438,9 @@ tt_status na2c_search(const Space& sp, const State& s0, uint64_t budget, const t
       }
       push_trace(out, evals, now_s() - t0, s2, c, out->best_cost);
       ++evals;
+      if (o.train_per_candidate) train();                                 // line 24, inside the loop
     }
-    // line 24: train once per batch (Z18)
-    const size_t n = memory.size();
-    if (n > 0) {
-      std::vector<std::vector<double>> gWc, gbc, gWa, gba;
-      for (int ep = 0; ep < epochs; ++ep) {
-        std::vector<size_t> mb(minibatch);
-        for (int b = 0; b < minibatch; ++b) mb[b] = (size_t)rng_nn.bounded(n);
-        critic.zero_like(gWc, gbc);
-        actor.zero_like(gWa, gba);
-        std::vector<double> adv(minibatch);
-        const double B = (double)minibatch;
-        for (int b = 0; b < minibatch; ++b) {
-          const Transition& tr = memory[mb[b]];
-          std::vector<double> xs(nin), x2(nin);
-          sp.features(tr.s, xs.data());
-          sp.features(tr.s2, x2.data());
-          critic.forward(x2.data(), &acts2);
-          const double v2 = acts2.back()[0];
-          critic.forward(xs.data(), &acts);
-          const double v = acts.back()[0];
-          adv[b] = tr.r + o.gamma * v2 - v;
-          const double dv = -2.0 * adv[b] / B;                            // d mean(A^2) / dV(s)
-          critic.backward(acts, &dv, gWc, gbc);
-        }
-        for (int b = 0; b < minibatch; ++b) {
-          const Transition& tr = memory[mb[b]];
-          std::vector<double> xs(nin);
-          sp.features(tr.s, xs.data());
-          actor.forward(xs.data(), &acts);
-          legal_mask(tr.s, &mask);
-          masked_softmax(acts.back(), mask, &pi);
-          double Hs = 0.0;
-          for (int i = 0; i < nact; ++i)
-            if (mask[i] && pi[i] > 0) Hs -= pi[i] * std::log(pi[i]);
-          std::vector<double> dz(nact, 0.0);
-          for (int i = 0; i < nact; ++i) {
-            if (!mask[i]) continue;
-            const double lp = pi[i] > 0 ? std::log(pi[i]) : 0.0;
-            double g = adv[b] * pi[i];                       // -A (onehot - pi), off-action part
-            if (i == tr.a) g -= adv[b];
-            g += o.beta * pi[i] * (lp + Hs);                 // -beta dH/dz
-            dz[i] = g / B;
-          }
-          actor.backward(acts, dz.data(), gWa, gba);
-        }
-        critic.sgd(gWc, gbc, o.lr, o.clip);
-        actor.sgd(gWa, gba, o.lr, o.clip);
-      }
-    }
+    if (!o.train_per_candidate) train();                                   // line 24, once per batch (Z18)
   }
   out->evals = evals;
   out->wall_s = now_s() - t0;

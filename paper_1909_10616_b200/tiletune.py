@@ -66,7 +66,8 @@ class SearchOpts(C.Structure):
                 ("measure", MeasureOpts), ("rho", i32), ("width", i32), ("steps_T", i32), ("epsilon", dbl),
                 ("batch", i32), ("mem_capacity", i32), ("gamma", dbl), ("beta", dbl), ("lr", dbl), ("clip", dbl),
                 ("epochs", i32), ("minibatch", i32), ("hidden", i32), ("rollout_cap_factor", i32),
-                ("max_t_increase", i32), ("steps_T_floor", i32), ("steps_T_decay_every", i32), ("layout", i32)]
+                ("max_t_increase", i32), ("steps_T_floor", i32), ("steps_T_decay_every", i32), ("layout", i32),
+                ("train_per_candidate", i32)]
 
 
 class LaunchInfo(C.Structure):
@@ -98,6 +99,7 @@ EXPORTS = {
     "tt_ctx_destroy": (i32, [vp]),
     "tt_ctx_stream": (i32, [vp, C.POINTER(vp)]),
     "tt_ctx_operands": (i32, [vp, i64, i64, i64, i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
+    "tt_aggregate": (i32, [C.POINTER(dbl), i32, C.POINTER(Sample)]),
     "tt_measure": (i32, [vp, C.POINTER(Space), C.POINTER(Config), C.POINTER(MeasureOpts), C.POINTER(Sample)]),
     "tt_gbfs_search": (i32, [vp, i64, i64, i64, u64, C.POINTER(SearchOpts), C.POINTER(Result),
                              C.POINTER(TraceRow), u64]),
@@ -256,6 +258,14 @@ def gemm(A, B, C_out, family: int, s: State, stream=None, layout: int = LAYOUT_N
     assert K == K2 and tuple(C_out.shape) == (M, N)
     _check(lib.tt_gemm_ex(M, N, K, family, layout, A.data_ptr(), B.data_ptr(), C_out.data_ptr(),
                           C.byref(to_config(s)), _stream(stream)), "gemm")
+
+
+def aggregate(per_repeat: Sequence[float]) -> Sample:
+    """The cost statistic tt_measure applies to its per-repeat means (tt_aggregate, reading Z10)."""
+    arr = (dbl * max(len(per_repeat), 1))(*per_repeat)
+    out = Sample()
+    _check(lib.tt_aggregate(arr, len(per_repeat), C.byref(out)), "aggregate")
+    return out
 
 
 def measure_opts(**kw) -> MeasureOpts:

@@ -4,6 +4,7 @@ import math
 import os
 import re
 
+import numpy as np
 import pytest
 
 from oracle import costs, gbfs as ogbfs, hw, na2c as ona2c, space
@@ -26,7 +27,7 @@ def test_abi_exports_every_declared_symbol():
     for name in sorted(declared):
         assert hasattr(tt.lib, name), name
     assert set(tt.EXPORTS) == declared
-    assert tt.lib.tt_version() == 4
+    assert tt.lib.tt_version() == 5
 
 
 @pytest.mark.parametrize("dims,d,fam", [((512, 512, 512), (4, 2, 4), 0), ((1024, 1024, 1024), (4, 2, 4), 0),
@@ -210,6 +211,9 @@ def test_na2c_eps0_small_batch_parity():
     (0, "t2", 200, {}),
     (1, "t1", 200, {}),
     (2, "t2", 160, {"batch": 8, "steps": 2, "gamma": 0.5}),
+    # Alg. 2's own placement of "Train ..." inside the "for s' in B_collect" loop
+    (3, "t2", 96, {"train_per_candidate": True}),
+    (4, "t1", 80, {"train_per_candidate": True, "batch": 6}),
 ])
 def test_na2c_policy_trace_parity(seed, table, budget, kw):
     # epsilon = 0.8 (the policy is followed with probability eps): the actor is sampled
@@ -221,11 +225,16 @@ def test_na2c_policy_trace_parity(seed, table, budget, kw):
     tab = costs.table(sp, f)
     p = ona2c.Params(epsilon=0.8, **kw)
     o = ona2c.na2c(sp, ogbfs.table_source(sp, tab), budget=budget, params=p, seed=seed)
-    lo = {"batch": "batch", "steps": "steps_T", "gamma": "gamma"}
+    lo = {"batch": "batch", "steps": "steps_T", "gamma": "gamma", "train_per_candidate": "train_per_candidate"}
     lres = tt.na2c_search(64, 64, 64, budget, tt.search_opts(seed=seed, epsilon=0.8, **{lo[k]: v for k, v in kw.items()}),
                           table=tab)
     assert _trace_key(lres.trace) == _oracle_key(o)
     assert lres.best_cost == o.best_cost
+    if kw.get("train_per_candidate"):     # the placement of line 24 really changes the trajectory
+        kb = dict(kw, train_per_candidate=False)
+        ob = ona2c.na2c(sp, ogbfs.table_source(sp, tab), budget=budget, params=ona2c.Params(epsilon=0.8, **kb),
+                        seed=seed)
+        assert _oracle_key(ob) != _oracle_key(o)
 
 
 def test_na2c_policy_properties():
@@ -314,3 +323,20 @@ def test_umma_tail_split_policy(monkeypatch):
                       ((16, 1, 1, 128), (16, 128), (16, 1, 1, 128))).split_tiles == 0        # saving < 8 us
     monkeypatch.setenv("TT_TAIL_SPLIT", "0")
     assert tt.binding(sp, ((16, 2, 1, 128), (32, 128), (16, 1, 1, 256))).split_tiles == 0
+
+
+def test_aggregate_matches_oracle():
+    # a7 / reading Z10: the statistic tt_measure applies to its per-repeat event timings
+    # (tt_aggregate, the same host function) equals oracle/measure.py bit for bit on injected
+    # samples ("fake clock"), odd and even R, ties, R = 1, one outlier.
+    from oracle import measure
+    rng = np.random.default_rng(5)
+    cases = [[1.0, 2.0, 3.0, 4.0, 100.0, 5.0, 6.0, 7.0, 8.0, 9.0], [2.5], [3.0, 1.0, 2.0], [4.0, 4.0, 1.0, 4.0]]
+    cases += [list(rng.lognormal(-9, 0.3, size=R)) for R in (2, 5, 10, 11, 64)]
+    for xs in cases:
+        got = tt.aggregate(xs)
+        want = measure.aggregate(xs)
+        assert (got.cost_s, got.mean_s, got.min_s, got.stdev_s, got.repeats) == \
+            (want["cost"], want["mean"], want["min"], want["stdev"], want["repeats"]), xs
+    with pytest.raises(tt.TileTuneError):
+        tt.aggregate([])

@@ -36,6 +36,44 @@ def test_sample_without_replacement_uniform():
     assert sorted(SplitMix64(1).sample_indices(4, 9)) == [0, 1, 2, 3]   # all if |g| < rho (Z5)
 
 
+def _published():
+    with open(os.path.join(ROOT, "tests", "golden", "splitmix64.json")) as f:
+        g = json.load(f)
+    return g["seed"], [int(x) for x in g["outputs"]]
+
+
+def test_bounded_exact_from_published_vector():
+    # O7: bounded(n) = floor(next() * n / 2^64) (Lemire multiply-shift).  Expected values are
+    # derived here, by integer arithmetic, from the PUBLISHED outputs -- not from oracle.rng.
+    seed, outs = _published()
+    want = [(o * 26) >> 64 for o in outs]
+    assert want == [9, 4, 13, 6, 23]
+    assert want != [o % 26 for o in outs]              # a modulo reduction would fail here
+    r = SplitMix64(seed)
+    assert [r.bounded(26) for _ in range(5)] == want
+    # uniform() = (next() >> 11) 2^-53: the top 53 bits as an exact dyadic fraction
+    r = SplitMix64(seed)
+    assert [r.uniform() for _ in range(5)] == [(o >> 11) / float(1 << 53) for o in outs]
+
+
+def test_sample_indices_exact_from_published_vector():
+    # O7: partial Fisher-Yates, t = 0..r-1: j = t + bounded(L - t), swap idx[t], idx[j];
+    # L = 7, r = 3 worked by hand from the published outputs o0, o1, o2:
+    #   t=0: j = 0 + (o0 * 7 >> 64) = 2 -> [2,1,0,3,4,5,6]
+    #   t=1: j = 1 + (o1 * 6 >> 64) = 2 -> [2,0,1,3,4,5,6]
+    #   t=2: j = 2 + (o2 * 5 >> 64) = 4 -> [2,0,4,3,1,5,6]
+    seed, outs = _published()
+    assert [(outs[0] * 7) >> 64, (outs[1] * 6) >> 64, (outs[2] * 5) >> 64] == [2, 1, 2]
+    assert SplitMix64(seed).sample_indices(7, 3) == [2, 0, 4]
+    # rho >= L takes every index, in the shuffled order of a full Fisher-Yates
+    full = SplitMix64(seed).sample_indices(4, 9)
+    idx = [0, 1, 2, 3]
+    for t, o in zip(range(4), outs):
+        j = t + ((o * (4 - t)) >> 64)
+        idx[t], idx[j] = idx[j], idx[t]
+    assert full == idx
+
+
 def test_bounded_range_and_uniform():
     r = SplitMix64(11)
     xs = [r.bounded(26) for _ in range(26000)]
@@ -227,17 +265,117 @@ def test_mlp_clip():
     assert step <= 1.0 + 1e-12
 
 
-def test_advantage_gamma0_zero_critic():
-    # gamma = 0 and V == 0 -> A = r.  Check through Agent.train's formula on a 1-sample batch
+def _np_forward(Ws, bs, X):
+    """Plain forward pass written independently of oracle.mlp (numpy @, np.tanh)."""
+    h = X
+    for l, (W, b) in enumerate(zip(Ws, bs)):
+        z = h @ W.T + b
+        h = np.tanh(z) if l < len(Ws) - 1 else z
+    return h
+
+
+def _np_masked_log_softmax(z, mask):
+    zm = np.where(mask, z, -np.inf)
+    mx = zm.max()
+    lse = mx + np.log(np.exp(zm[mask] - mx).sum())
+    return np.where(mask, zm - lse, -np.inf)
+
+
+def _train_memory(sp, ag):
+    """A few predecessor transitions ("Store (s, a, r(s, a), s') to M") of two states."""
+    mem = []
+    for s2, r in ((((4, 4, 2, 2), (8, 8), (4, 4, 2, 2)), 1.7), (((2, 8, 2, 2), (16, 4), (8, 2, 2, 2)), 0.6)):
+        for t, (pred, a) in enumerate(space.predecessors(sp, s2)[:3]):
+            mem.append((pred, ag.acts.index(a), r * (1.0 + 0.25 * t), s2))
+    return mem
+
+
+@pytest.mark.parametrize("gamma,beta", [(0.9, 0.01), (0.0, 0.5), (0.9, 0.3)])
+def test_agent_train_is_sgd_on_stated_losses(gamma, beta):
+    """Pin of Agent.train (Alg. 2 line "Train actor's and critic's neural networks with M", P:327;
+    A2C, P:284 / S:400-406): one epoch with lr = 1 and clipping off must move every parameter by
+    minus the gradient of the stated losses over the drawn minibatch, computed here by central
+    finite differences with an independent numpy forward pass:
+        critic  L_c = mean_b (r_b + gamma V0(s'_b) - V(s_b))^2          (V0 = critic before the step)
+        actor   L_a = mean_b [-A_b log pi(a_b | s_b) - beta H(pi(. | s_b))],  A_b = r_b + gamma V0(s'_b) - V0(s_b)
+    with pi the softmax over the legitimate actions of s_b.  A flipped entropy sign, a dropped
+    factor 2 in dL_c/dV, or a wrong advantage fails this test."""
     sp = Spec(64, 64, 64)
-    p = na2c.Params(gamma=0.0)
-    ag = na2c.Agent(sp, p, SplitMix64(0))
-    for w in ag.critic.W + ag.critic.b:
-        w[...] = 0.0
-    x = np.array([space.features(sp, space.initial_state(sp))])
-    v, _ = ag.critic.forward(x)
-    r = 0.37
-    assert r + p.gamma * v[0, 0] - v[0, 0] == r
+    p = na2c.Params(gamma=gamma, beta=beta, lr=1.0, clip=0.0, epochs=1, minibatch=6, hidden=8)
+    rng_nn = SplitMix64(21)
+    ag = na2c.Agent(sp, p, rng_nn)
+    mem = _train_memory(sp, ag)
+    probe = SplitMix64(0)
+    probe.state = rng_nn.state                       # the same minibatch draws as train's
+    mb = [mem[probe.bounded(len(mem))] for _ in range(p.minibatch)]
+    Xs = np.array([space.features(sp, t[0]) for t in mb])
+    X2 = np.array([space.features(sp, t[3]) for t in mb])
+    r = np.array([t[2] for t in mb])
+    acts = [t[1] for t in mb]
+    masks = [ag.legal_mask(t[0]) for t in mb]
+    Wc0, bc0 = [w.copy() for w in ag.critic.W], [b.copy() for b in ag.critic.b]
+    Wa0, ba0 = [w.copy() for w in ag.actor.W], [b.copy() for b in ag.actor.b]
+    V0s = _np_forward(Wc0, bc0, Xs)[:, 0]
+    V0n = _np_forward(Wc0, bc0, X2)[:, 0]
+    target = r + gamma * V0n
+    adv = target - V0s
+
+    def loss_c(Ws, bs):
+        return float(np.mean((target - _np_forward(Ws, bs, Xs)[:, 0]) ** 2))
+
+    def loss_a(Ws, bs):
+        Z = _np_forward(Ws, bs, Xs)
+        tot = 0.0
+        for b in range(len(mb)):
+            lp = _np_masked_log_softmax(Z[b], masks[b])
+            pi = np.exp(lp[masks[b]])
+            H = -float((pi * lp[masks[b]]).sum())
+            tot += -adv[b] * lp[acts[b]] - beta * H
+        return tot / len(mb)
+
+    ag.train(mem, rng_nn)
+
+    def check(W0, b0, W1, b1, loss):
+        worst, gmax = 0.0, 0.0
+        for params0, params1 in ((W0, W1), (b0, b1)):
+            for l in range(len(params0)):
+                g_train = params0[l] - params1[l]              # = lr * grad with lr = 1
+                for idx in np.ndindex(params0[l].shape):
+                    Wp = [w.copy() for w in W0]
+                    bp = [b.copy() for b in b0]
+                    tgt = (Wp if params0 is W0 else bp)[l]
+                    h = 1e-6
+                    tgt[idx] += h
+                    lp_ = loss(Wp, bp)
+                    tgt[idx] -= 2 * h
+                    lm_ = loss(Wp, bp)
+                    fd = (lp_ - lm_) / (2 * h)
+                    worst = max(worst, abs(fd - g_train[idx]))
+                    gmax = max(gmax, abs(fd))
+        return worst, gmax
+
+    wc, gc = check(Wc0, bc0, ag.critic.W, ag.critic.b, loss_c)
+    wa, ga = check(Wa0, ba0, ag.actor.W, ag.actor.b, loss_a)
+    assert gc > 1e-3 and ga > 1e-3                                  # non-trivial gradients
+    assert wc <= 1e-7 + 1e-6 * gc, (wc, gc)
+    assert wa <= 1e-7 + 1e-6 * ga, (wa, ga)
+
+
+def test_advantage_gamma0_zero_critic():
+    # S:406: gamma = 0 and V == 0 -> A = r, so the actor step is the REINFORCE step on r.
+    # Through Agent.train: a zero critic stays zero-output only through its bias, so compare the
+    # actor update against the same train with gamma = 0.9 (V(s') = 0 makes gamma irrelevant).
+    sp = Spec(64, 64, 64)
+    outs = []
+    for g in (0.0, 0.9):
+        p = na2c.Params(gamma=g, lr=0.5, clip=0.0, epochs=1, minibatch=4, hidden=8)
+        rng = SplitMix64(3)
+        ag = na2c.Agent(sp, p, rng)
+        for w in ag.critic.W + ag.critic.b:
+            w[...] = 0.0
+        ag.train(_train_memory(sp, ag), rng)
+        outs.append([w.copy() for w in ag.actor.W])
+    assert all(np.array_equal(a, b) for a, b in zip(*outs))
 
 
 # ------------------------------------------------------------------ N-A2C (Alg. 2)
