@@ -182,7 +182,7 @@ typedef struct {
   int32_t reg_tile_m, reg_tile_n;   /* SIMT: per-thread register tile m3 x n3 */
   /* UMMA tail split: when the tile count is not a multiple of the co-resident
    * clusters, the last split_tiles tiles' k-blocks are shared by split_workers clusters (<= 4 per
-   * tile) and combined in descending-k order (store, then TMA reduce-adds); 0 = none. */
+   * tile) and combined in ascending-k order (the k-block-0 piece stores, the higher pieces TMA-reduce-add after every piece below them); 0 = none. */
   int32_t split_tiles, split_workers;
 } tt_launch_info;
 
@@ -243,7 +243,13 @@ tt_status tt_fill_uniform(void* dst, int32_t dtype, uint64_t seed, uint64_t idx0
  * BF16_UMMA.  Device pointers; launched on `stream`; never allocates, never synchronises.
  * The config's trip counts must tile M, N, K exactly (J_prod) and satisfy J_hw.
  * F32_SIMT keeps one fmaf chain per output in k order (bit-exact vs the oracle's fmaf mode).
- * Alignment: A, B, C 16-byte aligned; UMMA families need K and N multiples of 8 (bf16) / 4. */
+ * Alignment: A, B, C 16-byte aligned; UMMA families need K and N multiples of 8 (bf16) / 4.
+ * UMMA tail split (tt_launch_info.split_tiles > 0): the pieces of a split tile hand off through
+ * library-owned device words (a static array, one slice per launch stream, left zeroed by every
+ * launch), and a piece waits only on clusters with a lower index, so the launch needs no
+ * co-residency of its grid.  Two split launches that can overlap must use different streams; a
+ * captured graph keeps its capture stream's slice, so do not replay one graph concurrently on
+ * several streams (TT_TAIL_SPLIT=0 disables the split). */
 tt_status tt_gemm(int64_t M, int64_t N, int64_t K, int32_t family, const void* A, const void* B,
                   float* C, const tt_config* cfg, void* stream);
 

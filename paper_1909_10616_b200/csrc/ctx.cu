@@ -11,6 +11,8 @@
 #include <algorithm>
 #include <cmath>
 #include <map>
+#include <mutex>
+#include <set>
 #include <tuple>
 #include <vector>
 
@@ -44,6 +46,21 @@ tt_status launch_fill(void* dst, int dtype, uint64_t seed, uint64_t idx0, uint64
   const uint64_t blocks = std::min<uint64_t>((count + 255) / 256, 148ull * 16);
   k4_fill<<<(unsigned)blocks, 256, 0, stream>>>(dst, dtype, seed, idx0, count);
   return cuda_ok(cudaGetLastError(), err, "k4_fill") ? TT_OK : TT_E_CUDA;
+}
+
+bool ensure_max_smem(const void* fn, int bytes, std::string* err) {
+  static std::mutex mu;
+  static std::set<std::tuple<int, const void*, int>> done;
+  int dev = 0;
+  if (!cuda_ok(cudaGetDevice(&dev), err, "cudaGetDevice")) return false;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(dev, fn, bytes);
+  if (done.count(key)) return true;
+  if (!cuda_ok(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), err,
+               "cudaFuncSetAttribute(max dynamic shared memory)"))
+    return false;
+  done.insert(key);
+  return true;
 }
 
 tt_status bind(const Space& sp, const State& s, tt_launch_info* info, std::string* err) {
@@ -84,6 +101,22 @@ void aggregate_repeats(const double* per, int R, tt_sample* out) {
 
 // ---------------------------------------------------------------- ctx
 
+namespace {
+// Makes the ctx's device current for one call and restores the caller's device afterwards, so a
+// process can drive several GPUs through several contexts (and tt_gemm keeps the caller's device).
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t status;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    status = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+}  // namespace
+
 Ctx::~Ctx() {
   int prev = 0;
   cudaGetDevice(&prev);
@@ -112,7 +145,8 @@ Ctx::~Ctx() {
 }
 
 tt_status Ctx::init(std::string* err) {
-  if (!cuda_ok(cudaSetDevice(device), err, "cudaSetDevice")) return TT_E_CUDA;
+  DeviceGuard g(device);
+  if (!cuda_ok(g.status, err, "cudaSetDevice")) return TT_E_CUDA;
   if (!cuda_ok(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), err, "cudaStreamCreate")) return TT_E_CUDA;
   ev.resize(2 * kMaxRepeats + 2);
   for (auto& e : ev)
@@ -139,7 +173,8 @@ tt_status Ctx::operands(const Space& sp, Operands** out, std::string* err) {
   o.N = sp.dim[2];
   o.dtype = dtype;
   const size_t es = dtype == 1 ? 2 : 4;
-  if (!cuda_ok(cudaSetDevice(device), err, "cudaSetDevice")) return TT_E_CUDA;
+  DeviceGuard g(device);
+  if (!cuda_ok(g.status, err, "cudaSetDevice")) return TT_E_CUDA;
   if (!cuda_ok(cudaMalloc(&o.A, (size_t)o.M * o.K * es), err, "cudaMalloc(A)")) return TT_E_CUDA;
   if (!cuda_ok(cudaMalloc(&o.B, (size_t)o.K * o.N * es), err, "cudaMalloc(B)")) return TT_E_CUDA;
   if (!cuda_ok(cudaMalloc((void**)&o.C, (size_t)o.M * o.N * 4), err, "cudaMalloc(C)")) return TT_E_CUDA;
@@ -167,6 +202,8 @@ tt_status Ctx::flush_l2(std::string* err) {
 tt_status Ctx::measure(const Space& sp, const State& s, const tt_measure_opts& mo, tt_sample* out,
                        std::string* err) {
   NvtxRange nv("tt_measure");
+  DeviceGuard g(device);
+  if (!cuda_ok(g.status, err, "cudaSetDevice")) return TT_E_CUDA;
   Operands* o = nullptr;
   tt_status st = operands(sp, &o, err);
   if (st != TT_OK) return st;
@@ -274,7 +311,8 @@ tt_status Ctx::gemm_host(const Space& sp, const State& s, const void* Ah, const 
   const size_t es = sp.family == TT_FAM_BF16_UMMA ? 2 : 4;
   const size_t a = (size_t)sp.dim[0] * sp.dim[1] * es, b = (size_t)sp.dim[1] * sp.dim[2] * es,
                c = (size_t)sp.dim[0] * sp.dim[2] * 4;
-  if (!cuda_ok(cudaSetDevice(device), err, "cudaSetDevice")) return TT_E_CUDA;
+  DeviceGuard g(device);
+  if (!cuda_ok(g.status, err, "cudaSetDevice")) return TT_E_CUDA;
   auto grow = [&](void** p, size_t* cap, size_t need) {
     if (*cap >= need) return true;
     cudaFree(*p);

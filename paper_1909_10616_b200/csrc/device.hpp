@@ -39,4 +39,8 @@ inline bool cuda_ok(cudaError_t e, std::string* err, const char* what) {
   return false;
 }
 
+// Opt kernel `fn` into `bytes` of dynamic shared memory on the current device.  The attribute is
+// per device context, so the "already set" cache is keyed by (device, fn) and guarded by a lock.
+bool ensure_max_smem(const void* fn, int bytes, std::string* err);
+
 }  // namespace tt

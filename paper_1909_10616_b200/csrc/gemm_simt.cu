@@ -292,7 +292,6 @@ const FixedInst kFixed[] = {TT_FIXED3(4, 4), TT_FIXED3(4, 8), TT_FIXED3(8, 4)};
 
 struct Table {
   KernelFn fn[7][7] = {};
-  bool attr_set[7][7] = {};
   Table() { fill_all(fn, std::make_integer_sequence<int, 7>{}); }
 };
 Table& table() {
@@ -346,28 +345,17 @@ tt_status simt_launch(const Space& sp, const State& s, const float* A, const flo
     *err = "no SIMT kernel instance for this register tile";
     return TT_E_UNSUPPORTED;
   }
-  if (!tb.attr_set[lm][ln]) {
-    if (!cuda_ok(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemPerCta),
-                 err, "cudaFuncSetAttribute(k1_simt)"))
-      return TT_E_CUDA;
-    tb.attr_set[lm][ln] = true;
-  }
+  if (!ensure_max_smem((const void*)fn, kSmemPerCta, err)) return TT_E_CUDA;
   // TT_SIMT_FIXED=0 (experiments) keeps the generic instance for every config
   static const bool use_fixed = [] {
     const char* e = std::getenv("TT_SIMT_FIXED");
     return !(e && e[0] == '0');
   }();
   if (use_fixed) {
-    static bool fixed_attr[sizeof(kFixed) / sizeof(kFixed[0])] = {};
     for (size_t i = 0; i < sizeof(kFixed) / sizeof(kFixed[0]); ++i) {
       const FixedInst& f = kFixed[i];
       if (f.tm == li.reg_tile_m && f.tn == li.reg_tile_n && f.bk == li.tile_k && li.block_x <= f.lb) {
-        if (!fixed_attr[i]) {
-          if (!cuda_ok(cudaFuncSetAttribute((const void*)f.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            kSmemPerCta), err, "cudaFuncSetAttribute(k1_simt fixed)"))
-            return TT_E_CUDA;
-          fixed_attr[i] = true;
-        }
+        if (!ensure_max_smem((const void*)f.fn, kSmemPerCta, err)) return TT_E_CUDA;
         fn = f.fn;
         break;
       }

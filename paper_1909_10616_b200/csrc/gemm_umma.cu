@@ -67,7 +67,7 @@ struct UmmaArgs {
   // tail split: the last sk_tiles tiles' k-blocks are spread evenly over the
   // first sk_workers clusters; the remaining dp_tiles tiles go round-robin to all clusters.
   int dp_tiles, sk_tiles, sk_workers;
-  uint32_t* flags;                  // per split tile and CTA rank: completed-writer count x 4
+  int flag_group;                   // slice of g_split_flags this launch uses (per launch stream)
   uint64_t* trace;                  // debug (TT_UMMA_TRACE): per cluster x item timestamps, or null
 };
 
@@ -75,6 +75,15 @@ struct UmmaArgs {
 // t(MMA start), t(MMA last issue), t(epilogue: accumulator ready), t(epilogue: flag ok), t(done),
 // and in slot 7: kernel entry (item 0) / teardown barrier passed (item 1)
 constexpr int kTraceItems = 16;
+
+// Tail-split handshake words: per split tile and CTA rank, the number of epilogue warps of the
+// tile's pieces that have landed.  A module-scope device array (zero at module load, one copy per
+// device context), so tt_gemm never allocates or memsets; every launch leaves its words at zero
+// (the top piece resets them), so back-to-back launches and CUDA-graph replays need no reset.
+// Launches on different streams use different groups (host: split_flag_group).
+constexpr int kFlagGroups = 64;
+constexpr int kFlagWords = 1024;    // >= max split tiles (< 148 clusters) x CTAs per cluster (<= 4)
+__device__ uint32_t g_split_flags[kFlagGroups * kFlagWords];
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -139,8 +148,8 @@ __device__ __forceinline__ uint32_t atom_add_release(uint32_t* p, uint32_t v) {
   asm volatile("atom.release.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
 }
-// Spin until *flag >= target (written by the co-resident cluster that owns the higher k-blocks
-// of the same tile); the watchdog turns a lost writer into a trap instead of a hang.
+// Spin until *flag >= target (written by the lower-index clusters that own the lower k-blocks of
+// the same tile, see Sched); the watchdog turns a lost writer into a trap instead of a hang.
 __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target) {
   if (ld_acquire(flag) >= target) return;
   const uint64_t t0 = globaltimer();
@@ -288,47 +297,58 @@ template <int KIND>
 __device__ __forceinline__ constexpr uint32_t kind_sbo_mn() { return KIND == 1 ? 4u * 128u : 8u * 128u; }
 
 // One unit of work for a cluster: k-blocks [kb0, kb1) of output tile `tile`.  A split tile's
-// partial sums are combined in descending-k order: the piece holding the last k-block (order 0)
-// stores C, each lower piece waits until the pieces above it have landed and adds with a TMA
-// reduce.  Every role warp walks the identical sequence.
+// partial sums are combined in ascending-k order: the piece holding k-block 0 (order 0) stores C,
+// each higher piece waits until every piece below it has landed and adds with a TMA reduce.
+// Every role warp walks the identical sequence.
+//
+// Deadlock freedom.  Worker (cluster) w owns the contiguous k-block range [sk_begin(w),
+// sk_begin(w+1)) of the tail tiles in tile-major order, so the pieces below a piece of w belong
+// to clusters with a LOWER index.  A worker's range spans at most two tiles (its length is at most
+// k0) and it processes them last tile first: the first item is the piece that starts at k-block 0
+// of its tile (stores, waits on nobody) unless the range lies inside one tile, in which case it is
+// the worker's only item.  Hence every piece waits only on the first item of lower-index clusters,
+// which themselves wait only on lower indices: no cycles, and no wait on a cluster that is
+// dispatched later.  Clusters are dispatched in index order, so the tail split needs no
+// co-residency of the whole grid (concurrent kernels, MPS or green contexts that hold SMs only
+// delay it) -- the property CUB's decoupled look-back scan also relies on.
 struct Item {
   int tile, kb0, kb1, order;
   bool split;
 };
 
 struct Sched {
-  int w, P, dp;
-  int64_t pos, end;
+  int w, P, dp, nseg, seg;
+  int64_t b, e;
   __device__ __forceinline__ static int64_t sk_begin(const UmmaArgs& p, int v) {
     return (int64_t)v * ((int64_t)p.sk_tiles * p.k0) / p.sk_workers;
   }
-  __device__ __forceinline__ Sched(const UmmaArgs& p, int w_, int P_) : w(w_), P(P_), dp(w_), pos(0), end(0) {
+  __device__ __forceinline__ Sched(const UmmaArgs& p, int w_, int P_) : w(w_), P(P_), dp(w_), nseg(0), seg(0), b(0), e(0) {
     if (w < p.sk_workers) {
-      pos = sk_begin(p, w);
-      end = sk_begin(p, w + 1);
+      b = sk_begin(p, w);
+      e = sk_begin(p, w + 1);
+      if (e > b) nseg = (int)((e - 1) / p.k0 - b / p.k0) + 1;
     }
   }
-  // tail pieces first (their cross-cluster waits resolve while the data-parallel tiles run)
+  // tail pieces first, last tile of the range first; then the data-parallel tiles
   __device__ __forceinline__ bool next(const UmmaArgs& p, Item* it) {
-    if (pos < end) {
-      const int64_t t_rel = pos / p.k0;
-      const int kb0 = (int)(pos - t_rel * p.k0);
-      const int kb1 = (int)min((int64_t)p.k0, (int64_t)kb0 + (end - pos));
+    if (seg < nseg) {
+      const int64_t t_rel = (e - 1) / p.k0 - seg;
+      const int64_t ts = t_rel * p.k0;
+      const int64_t lo = b > ts ? b : ts;
+      const int64_t hi = e < ts + p.k0 ? e : ts + p.k0;
       it->tile = p.dp_tiles + (int)t_rel;
-      it->kb0 = kb0;
-      it->kb1 = kb1;
-      it->split = !(kb0 == 0 && kb1 == p.k0);
-      int order = 0;
-      if (it->split) {
-        const int64_t tend = (t_rel + 1) * p.k0;
-        for (int v = w + 1; v < p.sk_workers; ++v) {
-          const int64_t b = sk_begin(p, v);
-          if (b >= tend) break;
-          if (sk_begin(p, v + 1) > b) ++order;
+      it->kb0 = (int)(lo - ts);
+      it->kb1 = (int)(hi - ts);
+      it->split = !(it->kb0 == 0 && it->kb1 == p.k0);
+      int order = 0;                                 // pieces of this tile below this one
+      if (it->split)
+        for (int v = w - 1; v >= 0; --v) {
+          const int64_t vb = sk_begin(p, v), ve = sk_begin(p, v + 1);
+          if (ve <= ts) break;
+          if (ve > vb) ++order;
         }
-      }
       it->order = order;
-      pos += kb1 - kb0;
+      ++seg;
       return true;
     }
     if (dp < p.dp_tiles) {
@@ -592,8 +612,9 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                          ? p.trace + ((int64_t)cluster_id * kTraceItems + item_no) * 8 : nullptr;
       ++item_no;
       const int tm = it.tile % p.m0, tn = it.tile / p.m0;
-      uint32_t* flag = it.split ? p.flags + (it.tile - p.dp_tiles) * csize + crank : nullptr;
-      const bool add = it.split && it.order > 0;           // lower k-blocks: add onto C
+      uint32_t* flag = it.split ? g_split_flags + (size_t)p.flag_group * kFlagWords + (it.tile - p.dp_tiles) * csize + crank
+                                : nullptr;
+      const bool add = it.split && it.order > 0;           // higher k-blocks: add onto C
       mbar_wait(tfull0 + 8u * acc, aphase);
       tc_fence_after();
       if (tr) {
@@ -602,7 +623,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
         tr[4] = globaltimer();
       }
       if (add) {
-        wait_flag(flag, (uint32_t)kEpiWarps * (uint32_t)it.order);   // every epilogue warp of each piece above
+        wait_flag(flag, (uint32_t)kEpiWarps * (uint32_t)it.order);   // every epilogue warp of each piece below
         fence_proxy_async_global();
       }
       if (tr) tr[5] = globaltimer();
@@ -666,7 +687,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
         __syncwarp();
         if (lane == 0) {
           const uint32_t old = atom_add_release(flag, 1u);
-          if (it.kb0 == 0 && old == (uint32_t)kEpiWarps * ((uint32_t)it.order + 1u) - 1u) *flag = 0u;   // last piece: reset
+          if (it.kb1 == p.k0 && old == (uint32_t)kEpiWarps * ((uint32_t)it.order + 1u) - 1u) *flag = 0u;   // top piece lands last: reset
         }
       }
       if (tr) {
@@ -733,18 +754,16 @@ bool make_map(CUtensorMap* m, int kind, const void* ptr, uint64_t inner, uint64_
 }
 
 int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
   }
-  return n;
+  return n > 0 ? n : 148;
 }
 
 // Tail split policy: at most kMaxPieces clusters share one tile, so the
-// descending-k chain of TMA reduce-adds per tile stays short.  TT_TAIL_SPLIT = 0 disables it,
+// ascending-k chain of TMA reduce-adds per tile stays short.  TT_TAIL_SPLIT = 0 disables it,
 // 2 forces it wherever tiles % clusters != 0 (tests), unset / 1 = the measured policy in plan_of.
 // Read at every plan so a process can A/B both schedules.
 constexpr int kMaxPieces = 4;
@@ -757,15 +776,7 @@ int tail_split_mode() {
 
 template <int KIND, int CG>
 bool set_smem_attr(std::string* err) {
-  static bool done = false;
-  if (!done) {
-    if (!cuda_ok(cudaFuncSetAttribute((const void*)&k_umma<KIND, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kSmemPerCta),
-                 err, "cudaFuncSetAttribute(k_umma)"))
-      return false;
-    done = true;
-  }
-  return true;
+  return ensure_max_smem((const void*)&k_umma<KIND, CG>, kSmemPerCta, err);
 }
 
 template <int KIND, int CG>
@@ -813,24 +824,22 @@ int max_active_clusters(int kind, int cg, int csize, int smem) {
   return n;
 }
 
-// Per (device, stream) flag words of the tail split, allocated on first use and left zeroed by
-// every launch (the last piece of each tile resets its word), so CUDA-graph replays and
-// back-to-back launches on one stream need no memset; launches on different streams never share.
-uint32_t* split_flags(cudaStream_t stream, std::string* err) {
+// Flag group of a launch stream (g_split_flags): streams are numbered round-robin on first use,
+// per device.  Two split launches that may run concurrently must be on different streams (more
+// than kFlagGroups live streams wrap around); a CUDA graph keeps the group of its capture stream,
+// so replays of one graph must not overlap each other on several streams.
+int split_flag_group(cudaStream_t stream) {
   static std::mutex mu;
-  static std::map<std::pair<int, cudaStream_t>, uint32_t*> flags;
+  static std::map<std::pair<int, cudaStream_t>, int> groups;
+  static std::map<int, int> next;
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(mu);
-  auto& f = flags[{dev, stream}];
-  if (!f) {
-    void* ptr = nullptr;
-    const size_t bytes = sizeof(uint32_t) * 2 * 1024;
-    if (!cuda_ok(cudaMalloc(&ptr, bytes), err, "cudaMalloc(split flags)")) return nullptr;
-    if (!cuda_ok(cudaMemset(ptr, 0, bytes), err, "cudaMemset(split flags)")) return nullptr;
-    f = static_cast<uint32_t*>(ptr);
-  }
-  return f;
+  auto it = groups.find({dev, stream});
+  if (it != groups.end()) return it->second;
+  const int g = next[dev]++ % kFlagGroups;
+  groups[{dev, stream}] = g;
+  return g;
 }
 
 struct Plan {
@@ -946,8 +955,11 @@ tt_status launch_t(const Plan& pl, const CUtensorMap& ma, const CUtensorMap& mb,
   cfg.numAttrs = 1;
   UmmaArgs a = pl.a;
   if (a.sk_tiles) {
-    a.flags = split_flags(stream, err);
-    if (!a.flags) return TT_E_CUDA;
+    if (a.sk_tiles * pl.csize > kFlagWords) {
+      *err = "tail split wider than the flag array";
+      return TT_E_UNSUPPORTED;
+    }
+    a.flag_group = split_flag_group(stream);
   }
   static const char* trace_path = std::getenv("TT_UMMA_TRACE");
   const size_t trace_words = (size_t)(pl.grid / CG) * kTraceItems * 8;

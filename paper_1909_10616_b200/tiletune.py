@@ -247,15 +247,50 @@ def fill_uniform(tensor, seed: int, idx0: int = 0, stream=None):
     _check(lib.tt_fill_uniform(tensor.data_ptr(), dt, seed, idx0, tensor.numel(), _stream(stream)), "fill_uniform")
 
 
-def gemm(A, B, C_out, family: int, s: State, stream=None, layout: int = LAYOUT_NN):
-    """C_out[M,N] (fp32) = A[M,K] . B[K,N] with config s on the device (tt_gemm_ex).  With
-    layout=LAYOUT_TN, A is passed as W = A^T of shape [K, M] (P:372 Y = W^T X)."""
+def _operand_dtype(family: int):
+    import torch
+    if family == FAM_BF16_UMMA:
+        return torch.bfloat16
+    if family in (FAM_F32_SIMT, FAM_TF32_UMMA):
+        return torch.float32
+    raise ValueError(f"family {family} has no kernel")
+
+
+def _check_gemm_operands(A, B, C_out, family: int, layout: int, on_device: bool):
+    """The C-ABI sees raw pointers only, so this binding is the one place that can reject a wrong
+    dtype (a bf16 buffer read as fp32 runs past its end), a strided view, a mismatched shape or a
+    tensor on another device before the library reads or writes it.  Returns (M, N, K)."""
+    import torch
+    want = _operand_dtype(family)
+    named = (("A", A, want), ("B", B, want), ("C", C_out, torch.float32))
+    for name, t, dt in named:
+        if t.dtype != dt:
+            raise TypeError(f"{name} must be {dt} for family {family}, got {t.dtype}")
+    for name, t, _ in named:
+        if t.dim() != 2 or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous 2-D tensor (row-major), got shape "
+                             f"{tuple(t.shape)} strides {t.stride()}")
+        if on_device and not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor")
+        if not on_device and t.is_cuda:
+            raise ValueError(f"{name} must be a host tensor")
+    if on_device and not (A.device == B.device == C_out.device):
+        raise ValueError(f"A, B, C on different devices: {A.device}, {B.device}, {C_out.device}")
     if layout == LAYOUT_TN:
         K, M = A.shape
     else:
         M, K = A.shape
     K2, N = B.shape
-    assert K == K2 and tuple(C_out.shape) == (M, N)
+    if K != K2 or tuple(C_out.shape) != (M, N):
+        raise ValueError(f"shapes do not chain: A {tuple(A.shape)} (layout {layout}), B {tuple(B.shape)}, "
+                         f"C {tuple(C_out.shape)}")
+    return M, N, K
+
+
+def gemm(A, B, C_out, family: int, s: State, stream=None, layout: int = LAYOUT_NN):
+    """C_out[M,N] (fp32) = A[M,K] . B[K,N] with config s on the device (tt_gemm_ex).  With
+    layout=LAYOUT_TN, A is passed as W = A^T of shape [K, M] (P:372 Y = W^T X)."""
+    M, N, K = _check_gemm_operands(A, B, C_out, family, layout, on_device=True)
     _check(lib.tt_gemm_ex(M, N, K, family, layout, A.data_ptr(), B.data_ptr(), C_out.data_ptr(),
                           C.byref(to_config(s)), _stream(stream)), "gemm")
 
@@ -312,8 +347,7 @@ class Context:
         return out
 
     def gemm_host(self, A_host, B_host, C_host, family: int, s: State, layout: int = LAYOUT_NN):
-        M, K = A_host.shape if layout == LAYOUT_NN else A_host.shape[::-1]
-        _, N = B_host.shape
+        M, N, K = _check_gemm_operands(A_host, B_host, C_host, family, layout, on_device=False)
         _check(lib.tt_gemm_host(self.h, M, N, K, family, layout, A_host.data_ptr(), B_host.data_ptr(),
                                 C_host.data_ptr(), C.byref(to_config(s))), "gemm_host")
 
@@ -422,8 +456,12 @@ def im2col(x, R, S, stride=1, pad=0, out=None, stream=None):
     import torch
     Nb, Cc, H, W = x.shape
     P, Q = conv_out_hw(H, W, R, S, stride, pad)
+    if not (x.is_cuda and x.is_contiguous()):
+        raise ValueError("im2col needs a contiguous NCHW CUDA tensor")
     if out is None:
         out = torch.empty(Nb * P * Q, Cc * R * S, device=x.device, dtype=x.dtype)
+    elif not (out.is_contiguous() and out.dtype == x.dtype and out.numel() == Nb * P * Q * Cc * R * S):
+        raise ValueError("im2col out must be contiguous, of x's dtype and [Nb*P*Q, C*R*S] elements")
     dt = {torch.float32: 0, torch.bfloat16: 1}[x.dtype]
     _check(lib.tt_im2col(dt, x.data_ptr(), Nb, Cc, H, W, R, S, stride, pad, out.data_ptr(), _stream(stream)),
            "im2col")
@@ -434,8 +472,15 @@ def conv2d(x, Wm, family: int, s: State, R: int, S: int, stride=1, pad=0, worksp
     """Conv layer through im2col + the tiled GEMM: returns y [Nb*P*Q, Kf] fp32 (tt_conv2d);
     Wm is the kernel matrix [C*R*S, Kf]."""
     import torch
+    want = _operand_dtype(family)
+    if x.dtype != want or Wm.dtype != want or not x.is_contiguous() or not Wm.is_contiguous():
+        raise TypeError(f"conv2d with family {family} needs contiguous {want} x and Wm")
+    if not (x.is_cuda and Wm.is_cuda and x.device == Wm.device):
+        raise ValueError("x and Wm must be CUDA tensors on one device")
     Nb, Cc, H, W = x.shape
     M, Kf, K = conv_gemm_dims(x.shape, Wm.shape[1], R, S, stride, pad)
+    if Wm.dim() != 2 or Wm.shape[0] != K:
+        raise ValueError(f"kernel matrix must be [C*R*S, Kf] = [{K}, Kf], got {tuple(Wm.shape)}")
     if workspace is None:
         workspace = torch.empty(M * K, device=x.device, dtype=x.dtype)
     y = torch.empty(M, Kf, device=x.device, dtype=torch.float32)

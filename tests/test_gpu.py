@@ -459,3 +459,142 @@ def test_simt_unaligned_views():
     with pytest.raises(tt.TileTuneError):
         tt.gemm(to_dev(A, True)[:, :].contiguous(), Bbuf[1:].view(K, N).to(torch.bfloat16), torch.empty(M, N, device=DEV),
                 tt.FAM_BF16_UMMA, ((1, 1, 1, 128), (2, 16), (1, 1, 1, 64)))
+
+
+# ------------------------------------------------------------------ round 2: full-size parity holes
+def _tail_rows(sp_lib, cfg, M):
+    """Rows to check for a config at full size: the first / last row and one row of every row
+    block that holds a tile of the tail split (the last split_tiles tiles)."""
+    info = tt.binding(sp_lib, cfg)
+    m0 = cfg[0][0]
+    tiles = m0 * cfg[2][0]
+    rows = {0, M - 1}
+    for t in range(tiles - info.split_tiles, tiles):
+        tm = t % m0
+        rows.add(tm * info.tile_m + (37 * t) % info.tile_m)
+    return info, np.array(sorted(rows))
+
+
+@pytest.mark.parametrize("fam,cfg", [
+    (3, ((16, 2, 1, 128), (32, 128), (16, 1, 1, 256))),    # bf16 4096^3 driver-bench config (r1 BENCH)
+    (3, ((8, 2, 2, 128), (64, 64), (16, 1, 1, 256))),      # bf16 4096^3 round-2 baseline best
+    (2, ((8, 2, 2, 128), (128, 32), (16, 1, 1, 256))),     # tf32 4096^3 best (profiles/r7_workloads)
+])
+def test_umma_best_configs_4096_default_policy(fam, cfg):
+    # the reported 4096^3 launches under the DEFAULT tail-split policy, rows crossing the split tiles
+    M = N = K = 4096
+    bf16 = fam == tt.FAM_BF16_UMMA
+    sp_lib = tt.make_space(M, N, K, family=fam)
+    info, rows = _tail_rows(sp_lib, cfg, M)
+    A, B = host_inputs(M, N, K, bf16=bf16)
+    C = run(fam, cfg, A, B)
+    R = og.gemm_f64_rows(A, B, rows)
+    assert og.normwise_error(C[rows], R) <= 5e-3, (cfg, info.split_tiles)
+    assert not np.isnan(C).any()
+    if fam == tt.FAM_BF16_UMMA and cfg[1] == (32, 128):
+        assert info.split_tiles > 0                       # the driver's headline launch splits its tail
+
+
+def test_simt_best_config_4096_sampled_rows():
+    # K1's reported 4096^3 config (profiles/r7_workloads/bench_f32_4096.json): fmaf-bit-exact rows
+    M = N = K = 4096
+    s = ((64, 2, 2, 16), (128, 32), (16, 16, 2, 8))
+    A, B = host_inputs(M, N, K)
+    C = run(tt.FAM_F32_SIMT, s, A, B)
+    rows = np.array([0, 1, 63, 64, 2047, 4000, 4095])
+    assert np.array_equal(C[rows], og.gemm_fmaf(A[rows], B))
+    assert og.normwise_error(C[rows], og.gemm_f64_rows(A, B, rows)) <= 1e-4
+
+
+@pytest.mark.parametrize("fam,cfg,split", [
+    (1, ((8, 2, 4, 4), (512, 32), (8, 2, 4, 4)), "1"),
+    (1, ((4, 4, 2, 8), (128, 128), (16, 2, 4, 2)), "1"),
+    (3, ((2, 1, 1, 128), (256, 64), (2, 1, 1, 128)), "1"),
+    (3, ((1, 2, 1, 128), (128, 128), (1, 1, 1, 256)), "2"),   # forced split: 1 pair tile over many clusters
+    (2, ((2, 1, 1, 128), (512, 32), (2, 1, 1, 128)), "1"),
+    (2, ((1, 2, 1, 128), (256, 64), (2, 1, 1, 128)), "2"),
+])
+def test_k16384_all_families(fam, cfg, split, monkeypatch):
+    # the north star's tolerance clause holds "at K <= 16384": the longest K, full oracle
+    monkeypatch.setenv("TT_TAIL_SPLIT", split)
+    M, N, K = 256, 256, 16384
+    assert space.legitimate(Spec(M, K, N, family=fam), cfg)
+    bf16 = fam == tt.FAM_BF16_UMMA
+    A, B = host_inputs(M, N, K, bf16=bf16)
+    C = run(fam, cfg, A, B)
+    R = og.gemm_f64(A, B)
+    if fam == tt.FAM_F32_SIMT:
+        assert np.array_equal(C, og.gemm_fmaf(A, B))
+        assert og.normwise_error(C, R) <= 1e-4
+    else:
+        assert og.normwise_error(C, R) <= 5e-3
+        if split == "2":
+            assert tt.binding(tt.make_space(M, N, K, family=fam), cfg).split_tiles > 0
+
+
+def test_na2c_T_decay_device_replay():
+    # f1 (P:336 "the exploration step T can have a decay process"): live N-A2C with T decaying
+    # 4 -> 1 every 2 episodes, and Alg. 2's in-loop training (P:327), on the device cost source;
+    # the oracle's Algorithm 2 replayed on the recorded (state -> cost) table takes the same path
+    sp = Spec(512, 512, 512, family=1)
+    ctx = tt.Context(0)
+    for kw, okw in ((dict(steps_T=4, steps_T_floor=1, steps_T_decay_every=2, batch=8),
+                     dict(steps=4, steps_floor=1, decay_every=2, batch=8)),
+                    (dict(train_per_candidate=1, batch=8), dict(train_per_candidate=True, batch=8))):
+        res = tt.na2c_search(512, 512, 512, 40, tt.search_opts(family=1, seed=4, **kw), ctx=ctx)
+        assert res.evals == 40
+        table = {r["state"]: r["cost"] for r in res.trace}
+        o = ona2c.na2c(sp, lambda batch: [table[s] for s in batch], budget=40, params=ona2c.Params(**okw), seed=4)
+        assert [r.state for r in o.trace] == [r["state"] for r in res.trace]
+        assert o.best_cost == res.best_cost
+    ctx.close()
+
+
+def test_random_search_device_replay():
+    # f3 (P:64 "configurations are randomly selected to be tested"): the live random-search
+    # comparator on the bf16 tcgen05 space of 512^3; the oracle draws the same states in order
+    from oracle import random_search as ors
+    ctx = tt.Context(0)
+    res = tt.random_search(512, 512, 512, 40, tt.search_opts(family=3, seed=6, width=8), ctx=ctx)
+    ctx.close()
+    assert res.evals == 40 and res.space_feasible == 279
+    table = {r["state"]: r["cost"] for r in res.trace}
+    o = ors.random_search(Spec(512, 512, 512, family=3), lambda b: [table[s] for s in b], 40, seed=6, width=8)
+    assert [r.state for r in o.trace] == [r["state"] for r in res.trace]
+    assert o.best_cost == res.best_cost
+
+
+def test_umma_tail_split_beside_concurrent_kernel(monkeypatch):
+    # The tail split's pieces wait only on lower-index clusters (DESIGN.md §6), so it needs no
+    # co-residency of its whole grid.  Launch it while a long SIMT kernel on another stream holds
+    # the SMs (launched before and after it): it must complete, bit-identical to a lone launch.
+    monkeypatch.setenv("TT_TAIL_SPLIT", "2")
+    M = N = 2048
+    K = 512
+    cfg = ((16, 1, 1, 128), (8, 64), (16, 1, 1, 128))
+    A, B = host_inputs(M, N, K, bf16=True)
+    Ad, Bd = to_dev(A, True), to_dev(B, True)
+    alone = torch.full((M, N), float("nan"), device=DEV)
+    tt.gemm(Ad, Bd, alone, 3, cfg)
+    torch.cuda.synchronize()
+    assert tt.binding(tt.make_space(M, N, K, family=3), cfg).split_tiles > 0
+    # blocker: the untiled s0 of 1024^3 fp32 (P:369): 2^20 one-thread CTAs, tens of milliseconds
+    Xb = torch.ones(1024, 1024, device=DEV)
+    Yb = torch.ones(1024, 1024, device=DEV)
+    Zb = torch.empty(1024, 1024, device=DEV)
+    s0 = ((1024, 1, 1, 1), (1024, 1), (1024, 1, 1, 1))
+    sb, sg = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    for blocker_first in (True, False):
+        C = torch.full((M, N), float("nan"), device=DEV)
+        torch.cuda.synchronize()
+        if blocker_first:
+            tt.gemm(Xb, Yb, Zb, 1, s0, stream=sb)
+        tt.gemm(Ad, Bd, C, 3, cfg, stream=sg)
+        tt.gemm(Xb, Yb, Zb, 1, s0, stream=sb)
+        tt.gemm(Ad, Bd, C, 3, cfg, stream=sg)
+        torch.cuda.synchronize()
+        outs.append(C.cpu().numpy())
+    ref = alone.cpu().numpy()
+    assert all(np.array_equal(o, ref) for o in outs)
+    assert (Zb == 1024).all()

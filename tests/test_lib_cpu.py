@@ -340,3 +340,30 @@ def test_aggregate_matches_oracle():
             (want["cost"], want["mean"], want["min"], want["stdev"], want["repeats"]), xs
     with pytest.raises(tt.TileTuneError):
         tt.aggregate([])
+
+
+def test_binding_rejects_bad_operands():
+    # the ABI sees raw pointers only: the binding must stop wrong dtypes, strided views, shape
+    # mismatches and host tensors before the library reads or writes past a buffer (CPU-only check:
+    # every case raises before any library call)
+    import torch
+    cfg = ((2, 2, 4, 4), (4, 8), (2, 2, 4, 4))
+    A = torch.zeros(64, 32)
+    B = torch.zeros(32, 64)
+    C = torch.zeros(64, 64)
+    with pytest.raises(ValueError):                      # host tensors to the device entry point
+        tt.gemm(A, B, C, tt.FAM_F32_SIMT, cfg)
+    with pytest.raises(TypeError):                       # bf16 operands for the fp32 family
+        tt.gemm(A.bfloat16(), B.bfloat16(), C, tt.FAM_F32_SIMT, cfg)
+    with pytest.raises(TypeError):                       # fp32 operands for the bf16 family
+        tt.gemm(A, B, C, tt.FAM_BF16_UMMA, cfg)
+    with pytest.raises(TypeError):                       # C must be fp32
+        tt.gemm(A, B, C.bfloat16(), tt.FAM_F32_SIMT, cfg)
+    with pytest.raises(ValueError):                      # a transposed view is not row-major
+        tt.gemm(A, torch.zeros(64, 32).t(), C, tt.FAM_F32_SIMT, cfg)
+    ctx = object.__new__(tt.Context)
+    ctx.h = None
+    with pytest.raises(ValueError):                      # shapes that do not chain
+        tt.Context.gemm_host(ctx, A, torch.zeros(16, 64), C, tt.FAM_F32_SIMT, cfg)
+    with pytest.raises(TypeError):
+        tt.Context.gemm_host(ctx, A.double(), B, C, tt.FAM_F32_SIMT, cfg)
