@@ -8,16 +8,19 @@ configuration space explored.  Workload (default ``bf16_4096``, BASELINE configs
 at 4096^3 with bf16 operands and fp32 accumulation/output on the tcgen05 family (K3).
 
 One run does, in order:
- 1. the tuning pass (every SURVEY §8(a) row): space count / J_hw, G-BFS (Alg. 1, width W = 8,
-    rho = 5) with candidate batches measured by libtiletune's device evaluator -- sharded over
-    the ranks with an all_gather of the timings when N > 1 -- and the fraction explored;
+ 1. the tuning pass (every SURVEY §8(a) row): space count / J_hw, G-BFS (Alg. 1 with width
+    W = 16, rho = 5; reading Z9) with candidate rounds measured by libtiletune's device
+    evaluator (tt_measure_set) -- sharded over the ranks (LPT assignment, one all_reduce of the
+    costs per round) when N > 1 -- and the fraction explored;
  2. W untimed warm-up steps and K timed steps of the best-found GEMM, one launch per step on
     each rank's row shard (rank r owns A rows [4096 r, 4096 (r+1)), B replicated, no collective
     on the math path: weak scaling).  The L2 is flushed (256 MiB memset) before every step,
     outside the CUDA-event pair that times the launch; barrier + synchronize on both sides;
     the per-step time is the max over ranks.
  3. ``e2e``: the same GEMM through tt_gemm_host (pinned host A, B in; C out) per step;
- 4. ``cpu_baseline``: the oracle's double GEMM (oracle/gemm_ref.c) on a bounded row sample.
+ 4. ``fp32``: the paper's own arithmetic (fp32 FFMA, K1) on ``--fp32-workload`` (f32_2048):
+    G-BFS at 0.1 % of the raw space from the untiled s0, timed steps, fraction of the FFMA peak;
+ 5. ``cpu_baseline``: the oracle's double GEMM (oracle/gemm_ref.c) on a bounded row sample.
 
 ``--impl reference`` times the oracle alone (the reference arm of this tier), rank 0 only.
 """
@@ -222,6 +225,159 @@ def run_reference(args):
     }))
 
 
+def tune(ctx, sp, Mr, N, K, fam, layout, budget, args, world, coll, local):
+    """G-BFS over the config space with candidate rounds sharded over the ranks (SURVEY §8e);
+    candidates are scored under the timed region's protocol (L2 flushed before every timed
+    launch) so the search optimises what the bench reports.  Returns (best, tuning record)."""
+    from paper_1909_10616_b200 import dist as tdist
+    from paper_1909_10616_b200 import tiletune as tt
+    import torch.distributed as dist
+
+    raw, feasible = tt.count_configs(sp, feasible=True)
+    sopts = tt.search_opts(family=fam, seed=args.seed, width=args.width, layout=layout,
+                           measure={"l2_flush": 1 if args.tune_l2_flush else 0})
+    ms_fn, observe, cut_fn = tdist.device_measure_set(ctx, sp, sopts, device=local)
+    store = tdist.default_store() if (world > 1 and args.assign == "dynamic") else None
+    ev = tdist.TrackingEvaluator(observe=observe, measure_set=ms_fn, device=coll if world > 1 else None,
+                                 store=store, assign=None if store is not None else args.assign, space=sp,
+                                 cut_s=cut_fn)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    res = tt.gbfs_search(Mr, N, K, budget, sopts, batch=ev)
+    tune_wall = tdist.max_over_ranks(time.perf_counter() - t0, coll)
+    rec = {"algorithm": "G-BFS (Alg. 1, width %d, rho 5)" % args.width, "budget": budget, "evals": res.evals,
+           "space_raw": raw, "space_feasible": feasible, "frac_raw": res.frac_raw,
+           "frac_feasible": res.frac_feasible, "tuning_wall_s": tune_wall, "best_config": res.best,
+           "best_cost_us": res.best_cost * 1e6, "s0_cost_us": res.trace[0]["cost"] * 1e6,
+           "local_evals": ev.local_evals, "rounds": ev.rounds,
+           "scoring": ("L2 flushed before every timed launch" if args.tune_l2_flush else "warm L2, CUDA-graph replay")
+           + "; slow cut min(max(20 cost_min, 1 ms), 50 t_roof), racing at 1.25 cost_min (reading Z12)",
+           "assignment": ev.assign}
+    if world == 1:
+        # Projection of the sharded search (SURVEY §8e C4) from this run's per-candidate
+        # measurement times: each round's candidates assigned by rule, the slowest rank gates the
+        # round, + 50 us per round for the exchange; the host search work is replicated on every
+        # rank.  Not a multi-GPU measurement (the driver's N = 2/4/8 runs measure tuning_wall_s).
+        meas = sum(sum(t) for t in ev.round_times)
+        host = max(0.0, tune_wall - meas)
+        proj = {}
+        for G in (2, 4, 8):
+            ws = host + tdist.projected_sharded_wall(ev.round_times, G, per_round_s=50e-6)
+            wl = host + tdist.projected_sharded_wall(ev.round_times, G, per_round_s=50e-6, weights=ev.round_weights)
+            wd = host + tdist.projected_sharded_wall(ev.round_times, G, per_round_s=50e-6, dynamic=True,
+                                                     per_claim_s=200e-6)
+            proj[str(G)] = {"lpt_wall_s": wl, "lpt_speedup": tune_wall / wl if wl > 0 else None,
+                            "static_wall_s": ws, "static_speedup": tune_wall / ws if ws > 0 else None,
+                            "dynamic_wall_s": wd, "dynamic_speedup": tune_wall / wd if wd > 0 else None}
+        rec["projected_sharded_search"] = {"rounds": ev.rounds, "round_sizes": [len(t) for t in ev.round_times],
+                                           "measure_s": meas, "host_s": host, "by_gpus": proj,
+                                           "kind": "projection from 1-GPU per-candidate times"}
+    return res.best, rec
+
+
+def time_gemm(tt, A, B, C, fam, best, layout, steps, warmup, flush, world, sampler=None):
+    """W untimed + `steps` timed launches, L2 flushed before each (outside the event pair);
+    barrier + synchronize on both sides; returns per-step ms on the launching stream."""
+    import torch
+    import torch.distributed as dist
+    stream = torch.cuda.current_stream()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    for _ in range(warmup):
+        flush.fill_(1)
+        tt.gemm(A, B, C, fam, best, layout=layout)
+    torch.cuda.synchronize()
+    if sampler is not None:
+        sampler.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(steps):
+        flush.fill_(i & 0xFF)                           # L2 flush between steps (outside the events)
+        starts[i].record(stream)
+        tt.gemm(A, B, C, fam, best, layout=layout)
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    return [s.elapsed_time(e) for s, e in zip(starts, ends)]
+
+
+def spot_check(A_dev, C, Mr, N, K, r0, fam, tn):
+    """Untimed check of the timed output on sampled entries against the oracle's definition."""
+    import numpy as np
+
+    import synth
+    ii = np.array([0, Mr // 3, Mr - 1])
+    jj = np.array([N - 1, N // 2, 0])
+    if tn:
+        Wsh = synth.uniform_f32(1, K, Mr, row0=r0 * K // Mr)      # the rank's W block
+        Arows = np.stack([Wsh[:, int(i)] for i in ii])
+    else:
+        Arows = np.stack([synth.uniform_f32(1, 1, K, row0=r0 + int(i))[0] for i in ii])
+    Bh = synth.uniform_f32(2, K, N)
+    if fam == 3:
+        Arows = synth.bf16_bits_to_f32(synth.to_bf16_bits(Arows))
+        Bh = synth.bf16_bits_to_f32(synth.to_bf16_bits(Bh))
+    ref = np.array([float(np.dot(Arows[t].astype(np.float64), Bh[:, jj[t]].astype(np.float64))) for t in range(3)])
+    got = C.cpu().numpy()[ii, jj]
+    return float(np.max(np.abs(got - ref)) / max(1e-30, np.max(np.abs(ref))))
+
+
+def peak_of(fam, peaks, peak_src, sm_max_mhz):
+    if fam == 3:
+        return peaks["bf16_tflops"], f"bf16 dense, burst, {peak_src} (MEASURED_PEAKS.json)", "tensor"
+    if fam == 2:
+        return peaks["bf16_tflops"] * 0.5, f"tf32 = bf16 burst x 0.5 (nominal 1.1/2.25 ratio), {peak_src}", "tensor"
+    smx = sm_max_mhz or 1965.0
+    return (fp32_fma_peak_tflops(smx), f"fp32 FFMA: 148 SM x 128 lanes x 2 x {smx:.0f} MHz (DESIGN.md §6)", "alu")
+
+
+def traffic_of(workload, best):
+    """DRAM bytes per launch of this config from the committed ncu captures, or None."""
+    tp = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
+    if not os.path.exists(tp):
+        return None
+    with open(tp) as f:
+        tr = json.load(f)
+    want = [list(v) for v in best]
+    for e in tr.get("configs", [tr]):
+        if e.get("config") == want:
+            return e.get("dram_bytes_per_launch")
+    return None
+
+
+def fp32_record(ctx, args, world, coll, local, dev, peaks, peak_src, sm_max):
+    """The paper's own arithmetic (fp32 CUDA-core FFMA, reading Z13) on its square workload: G-BFS
+    at 0.1 % of the raw space from the untiled s0, then timed steps of the best
+    config, as a fraction of the FFMA peak."""
+    import torch
+
+    from paper_1909_10616_b200 import tiletune as tt
+    name = args.fp32_workload
+    Mr, N, K, fam, budget = WORKLOADS[name]
+    sp = tt.make_space(Mr, N, K, family=fam)
+    best, rec = tune(ctx, sp, Mr, N, K, fam, tt.LAYOUT_NN, budget, args, world, coll, local)
+    A = torch.empty(Mr, K, device=dev)
+    B = torch.empty(K, N, device=dev)
+    C = torch.empty(Mr, N, device=dev)
+    tt.fill_uniform(A, seed=1)
+    tt.fill_uniform(B, seed=2)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    per = time_gemm(tt, A, B, C, fam, best, tt.LAYOUT_NN, max(5, min(args.steps, 20)), 3, flush, world)
+    ms = statistics.mean(per)
+    flops = 2.0 * Mr * N * K
+    achieved = flops / (ms * 1e-3) / 1e12
+    peak, note, bound = peak_of(fam, peaks, peak_src, sm_max)
+    return {"workload": name, "family": "f32_simt", "value": achieved, "unit": "TFLOP/s", "ms_per_step": ms,
+            "best_config": {"m": list(best[0]), "k": list(best[1]), "n": list(best[2])},
+            "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "peak_source": note},
+            "tuning": rec, "spot_check_err": spot_check(A, C, Mr, N, K, 0, fam, False),
+            "l2": "flushed (256 MiB memset) before every timed launch"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
@@ -230,13 +386,19 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="bf16_4096", choices=sorted(WORKLOADS))
     ap.add_argument("--budget", type=int, default=None, help="G-BFS evaluation budget (distinct configs)")
-    ap.add_argument("--width", type=int, default=8)
+    ap.add_argument("--width", type=int, default=16,
+                    help="G-BFS states popped per round W (reading Z9): the same for every GPU count")
+    ap.add_argument("--assign", choices=["lpt", "static", "dynamic"], default="lpt",
+                    help="how a round's candidates are spread over the ranks (paper_1909_10616_b200/dist.py)")
     ap.add_argument("--layout", choices=["nn", "tn"], default="nn",
                     help="tn: A stored as W[K][M] (the paper's perceptron Y = W^T X, P:372)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--ref-rows", type=int, default=16)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fp32-workload", default="f32_2048", choices=[k for k in WORKLOADS if k.startswith("f32")],
+                    help="workload of the fp32 (paper arithmetic) record")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the fp32 record")
     ap.add_argument("--config", default=None, help="skip tuning and use this config (JSON triple)")
     ap.add_argument("--tune-warm", dest="tune_l2_flush", action="store_false",
                     help="score candidates warm (CUDA-graph replay) instead of with the timed region's L2 flush")
@@ -283,49 +445,13 @@ def main():
     ctx = tt.Context(local, input_seed=1)
     layout = tt.LAYOUT_TN if args.layout == "tn" else tt.LAYOUT_NN
     sp = tt.make_space(Mr, N, K, family=fam, layout=layout)
-    raw, feasible = tt.count_configs(sp, feasible=True)
 
     # ---------------- 1. tuning pass (G-BFS, candidates sharded over ranks) ----------------
     if args.config:
         best = tuple(tuple(v) for v in json.loads(args.config))
-        tune = None
+        tune_rec = None
     else:
-        # candidates are scored under the timed region's protocol (L2 flushed before every timed
-        # launch), so the search optimises what the bench reports
-        mo = tt.measure_opts(l2_flush=1 if args.tune_l2_flush else 0)
-        measure_one, observe = tdist.device_measure(ctx, sp, opts=mo)
-        ev = tdist.TrackingEvaluator(measure_one, observe, device=coll if world > 1 else None,
-                                     store=tdist.default_store() if world > 1 else None)
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        res = tt.gbfs_search(Mr, N, K, budget, tt.search_opts(family=fam, seed=args.seed, width=args.width, layout=layout), batch=ev)
-        tune_wall = tdist.max_over_ranks(time.perf_counter() - t0, coll)
-        best = res.best
-        tune = {"algorithm": "G-BFS (Alg. 1, width %d, rho 5)" % args.width, "budget": budget, "evals": res.evals,
-                "space_raw": raw, "space_feasible": feasible, "frac_raw": res.frac_raw,
-                "frac_feasible": res.frac_feasible, "tuning_wall_s": tune_wall, "best_config": best,
-                "best_cost_us": res.best_cost * 1e6, "s0_cost_us": res.trace[0]["cost"] * 1e6,
-                "local_evals": ev.local_evals, "scoring": "L2 flushed before every timed launch" if args.tune_l2_flush
-                else "warm L2, CUDA-graph replay", "assignment": "dynamic (TCPStore counter)" if ev.store is not None
-                else "static (j mod G)"}
-        if world == 1:
-            # Projection of the sharded search from this run's per-candidate
-            # measurement times: candidate j of a round on rank j mod G, the slowest rank gates
-            # the round, + 50 us per round for the all_gather; the host search work is
-            # replicated on every rank.  Not a multi-GPU measurement (the driver's N = 2/4/8 runs
-            # measure tuning_wall_s directly).
-            meas = sum(sum(t) for t in ev.round_times)
-            host = max(0.0, tune_wall - meas)
-            proj = {}
-            for G in (2, 4, 8):
-                ws = host + tdist.projected_sharded_wall(ev.round_times, G, per_round_s=50e-6)
-                wd = host + tdist.projected_sharded_wall(ev.round_times, G, per_round_s=50e-6, dynamic=True,
-                                                         per_claim_s=200e-6)
-                proj[str(G)] = {"static_wall_s": ws, "static_speedup": tune_wall / ws if ws > 0 else None,
-                                "dynamic_wall_s": wd, "dynamic_speedup": tune_wall / wd if wd > 0 else None}
-            tune["projected_sharded_search"] = {"rounds": ev.rounds, "measure_s": meas, "host_s": host,
-                                                "by_gpus": proj, "kind": "projection from 1-GPU per-candidate times"}
+        best, tune_rec = tune(ctx, sp, Mr, N, K, fam, layout, budget, args, world, coll, local)
     info = tt.binding(sp, best)
 
     # ---------------- 2. timed steps of the best-found GEMM on this rank's row shard ----------
@@ -340,54 +466,14 @@ def main():
     tt.fill_uniform(A, seed=1, idx0=r0 * K)        # NN: global row indices; TN: rank block offset
     tt.fill_uniform(B, seed=2)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    for _ in range(args.warmup):
-        flush.fill_(1)
-        tt.gemm(A, B, C, fam, best, layout=layout)
-    torch.cuda.synchronize()
     sampler = ClockSampler(local)
-    sampler.start()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    for i in range(args.steps):
-        flush.fill_(i & 0xFF)                           # L2 flush between steps (outside the events)
-        starts[i].record(stream)
-        tt.gemm(A, B, C, fam, best, layout=layout)
-        ends[i].record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    per = time_gemm(tt, A, B, C, fam, best, layout, args.steps, args.warmup, flush, world, sampler=sampler)
     clocks = sampler.stop()
-    per = [s.elapsed_time(e) for s, e in zip(starts, ends)]       # ms, launching stream
     ms_local = sum(per) / len(per)
     ms = tdist.max_over_ranks(ms_local, coll)
     flops_rank = 2.0 * Mr * N * K
     value = world * flops_rank / (ms * 1e-3) / 1e12                 # whole-job TFLOP/s
-
-    # spot-check the timed output against the oracle on sampled entries (untimed)
-    import numpy as np
-
-    import synth
-    from oracle import gemm as og
-    ii = np.array([0, Mr // 3, Mr - 1])
-    jj = np.array([N - 1, N // 2, 0])
-    Ah = synth.uniform_f32(1, 3, K, row0=0)
-    if tn:
-        Wsh = synth.uniform_f32(1, K, Mr, row0=r0 * K // Mr)      # the rank's W block
-        Arows = np.stack([Wsh[:, int(i)] for i in ii])
-    else:
-        Arows = np.stack([synth.uniform_f32(1, 1, K, row0=r0 + int(i))[0] for i in ii])
-    Bh = synth.uniform_f32(2, K, N)
-    if bf16:
-        Arows = synth.bf16_bits_to_f32(synth.to_bf16_bits(Arows))
-        Bh = synth.bf16_bits_to_f32(synth.to_bf16_bits(Bh))
-    ref = np.array([float(np.dot(Arows[t].astype(np.float64), Bh[:, jj[t]].astype(np.float64))) for t in range(3)])
-    got = C.cpu().numpy()[ii, jj]
-    spot_err = float(np.max(np.abs(got - ref)) / max(1e-30, np.max(np.abs(ref))))
-    del Ah
+    spot_err = spot_check(A, C, Mr, N, K, r0, fam, tn)
 
     # ---------------- 3. e2e through tt_gemm_host (pinned host buffers) -----------------------
     Ah_t = A.cpu().pin_memory()
@@ -405,21 +491,9 @@ def main():
     h2d = Ah_t.numel() * Ah_t.element_size() + Bh_t.numel() * Bh_t.element_size()
     d2h = Ch_t.numel() * 4
 
-    # ---------------- 4. roofline + cpu baseline (rank 0) --------------------------------------
+    # ---------------- 4. roofline, the paper's fp32 arithmetic, cpu baseline -------------------
     peaks, peak_src = load_peaks()
-    if fam == 3:
-        peak = peaks["bf16_tflops"]
-        peak_note = f"bf16 dense, burst, {peak_src} (MEASURED_PEAKS.json)"
-        bound = "tensor"
-    elif fam == 2:
-        peak = peaks["bf16_tflops"] * 0.5
-        peak_note = f"tf32 = bf16 burst x 0.5 (nominal 1.1/2.25 ratio), {peak_src}"
-        bound = "tensor"
-    else:
-        smx = clocks.get("sm_max_mhz") or 1965.0
-        peak = fp32_fma_peak_tflops(smx)
-        peak_note = f"fp32 FFMA: 148 SM x 128 lanes x 2 x {smx:.0f} MHz (DESIGN.md §6)"
-        bound = "alu"
+    peak, peak_note, bound = peak_of(fam, peaks, peak_src, clocks.get("sm_max_mhz"))
     achieved = flops_rank / (ms_local * 1e-3) / 1e12
     # memory side of the same launch: compulsory bytes (A, B in at the input width, C out fp32)
     in_bytes = 2 if fam == 3 else 4
@@ -428,13 +502,10 @@ def main():
                 "peak_gbs": peaks["hbm_gbs"], "frac": comp_bytes / (ms_local * 1e-3) / 1e9 / peaks["hbm_gbs"],
                 "t_floor_us": {"memory": comp_bytes / (peaks["hbm_gbs"] * 1e9) * 1e6,
                                "compute": flops_rank / (peak * 1e12) * 1e6}}
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
-    if os.path.exists(tp):
-        with open(tp) as f:
-            tr = json.load(f)
-        if tr.get("config") == [list(v) for v in best]:
-            traffic = tr.get("dram_bytes_per_launch")
+    traffic = traffic_of(args.workload, best)
+    fp32 = None
+    if not args.no_fp32 and fam != 1:
+        fp32 = fp32_record(ctx, args, world, coll, local, dev, peaks, peak_src, clocks.get("sm_max_mhz"))
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, sample = cpu_oracle_sample(Mr, N, K, fam, seconds=args.cpu_seconds)
@@ -453,12 +524,14 @@ def main():
                        "l2": "flushed (256 MiB memset) before every timed launch",
                        "best_config": {"m": list(best[0]), "k": list(best[1]), "n": list(best[2])},
                        "launch": {"grid": info.grid_x, "cluster": info.cluster_x, "tile": [info.tile_m, info.tile_n,
-                                  info.tile_k], "stages": info.stages, "smem": info.smem_bytes}},
-            "tuning": tune,
+                                  info.tile_k], "stages": info.stages, "smem": info.smem_bytes,
+                                  "split_tiles": info.split_tiles}},
+            "tuning": tune_rec,
             "pct_of_peak": 100.0 * achieved / peak,
             "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_note,
                          "algorithmic": f"2*M*N*K = {flops_rank:.4g} flop per launch", "hbm_side": hbm_side},
+            "fp32": fp32,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": "tt_gemm_host (pinned host A,B -> device -> C host)"},

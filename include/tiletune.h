@@ -83,7 +83,7 @@ typedef struct {
   int32_t device;          /* CUDA ordinal the sample was taken on */
   int32_t slow_cut;        /* 1 if cost_s = probe_s because probe_s > cut_s (Z12) */
   int32_t graph_nodes;     /* launches per captured CUDA graph the repeats replayed (0: direct launches) */
-  int32_t reserved;
+  int32_t raced;           /* 1 if the repeats stopped after race_repeats (tt_measure_opts.race_s) */
 } tt_sample;
 
 typedef struct {
@@ -96,6 +96,10 @@ typedef struct {
   int32_t graph;           /* 1 (default): each repeat replays a CUDA graph of up to 32 captured
                               launches, so host launch overhead never enters the score; 0: direct
                               launches from the host loop.  Ignored with l2_flush. */
+  double race_s;           /* if > 0: when the first race_repeats repeats all exceed race_s, stop
+                              there (cost = their median, raced = 1) -- a candidate that cannot
+                              beat the incumbent is not timed to full precision (reading Z12) */
+  int32_t race_repeats;    /* default 3 */
 } tt_measure_opts;
 
 /* One row per measured state, in evaluation order (Fig. 7 axes P:352). */
@@ -165,6 +169,12 @@ typedef struct {
    * "for s' in B_collect" loop.  1: train after every candidate, in that order;
    * 0 (default, reading Z18 / S:422): train once after each measured batch. */
   int32_t train_per_candidate;
+  /* Scoring budget of the DEVICE / batch cost sources (reading Z12, "searching time" P:359):
+   * cut_s = min(max(20 cost_min, 1 ms), max(1 ms, cut_roofline_x t_roof)), applied from s0 on
+   * (t_roof = tt_roofline_seconds), and race_s = race_factor cost_min.  cut_roofline_x <= 0 drops the
+   * absolute cut; race_factor <= 0 disables racing.  Defaults 50 and 1.25. */
+  double cut_roofline_x;
+  double race_factor;
 } tt_search_opts;
 
 /* How a config is bound to a launch (a5 of SURVEY §8a; for tests and reports). */
@@ -286,6 +296,24 @@ tt_status tt_ctx_operands(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, int32_t 
  * without J; TT_E_CUDA on a launch error. */
 tt_status tt_measure(tt_ctx* ctx, const tt_space* sp, const tt_config* cfg,
                      const tt_measure_opts* opts, tt_sample* out);
+
+/* One GEMM of sp at the family's nominal peak on `device` (-1: the current device; no device:
+ * 148 SMs at 1965 MHz): 2 M N K / (SMs x SM clock x flop/clk/SM), with 256 (fp32 FFMA: 128 lanes
+ * x 2), 4096 (TF32) and 8192 (BF16) flop/clk/SM.  The scale of the slow-candidate cut. */
+tt_status tt_roofline_seconds(const tt_space* sp, int32_t device, double* seconds);
+
+/* The per-candidate measurement options a search uses (reading Z12): copies opts->measure and
+ * sets cut_s and race_s from the incumbent cost_min (+inf before s0 is scored) as documented at
+ * tt_search_opts.cut_roofline_x.  Shared by the in-library DEVICE source and sharded evaluators. */
+tt_status tt_scoring_opts(const tt_space* sp, int32_t device, const tt_search_opts* opts, double cost_min,
+                          tt_measure_opts* out);
+
+/* Measure a set of candidates on the ctx device (the per-rank half of a sharded round, SURVEY
+ * §8e): for j in [0, n) with mine == NULL or mine[j] != 0, costs[j] = tt_measure(cfgs[j]).cost_s
+ * with `mo`, and secs[j] (nullable) = host wall seconds that measurement took; other entries are
+ * set to 0.  Stops at the first failing candidate (its status is returned). */
+tt_status tt_measure_set(tt_ctx* ctx, const tt_space* sp, const tt_config* cfgs, int32_t n, const uint8_t* mine,
+                         const tt_measure_opts* mo, double* costs, double* secs);
 
 /* The statistic tt_measure reports ("the arithmetic mean for 10 repeated trials"; reading
  * Z10): from R >= 1 per-repeat mean launch times per_repeat[0..R) (seconds, host array), sets

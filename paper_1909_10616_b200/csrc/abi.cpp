@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -59,9 +60,8 @@ tt_status run_search(SearchFn fn, tt_ctx* ctx, int64_t M, int64_t N, int64_t K, 
       if (!c) return fail(TT_E_INVAL, "DEVICE cost source needs a tt_ctx");
       if (sp->family == TT_FAM_NONE) return fail(TT_E_UNSUPPORTED, "family NONE has no kernel to measure");
       cost = [&](const std::vector<State>& cands, double inc, std::vector<double>* costs, std::string* err) {
-        tt_measure_opts mo = o->measure;
-        if (mo.cut_s == 0) mo.cut_s = std::isfinite(inc) ? std::max(20.0 * inc, 0.05) : 0.0;   // Z12
-        if (mo.cut_s < 0) mo.cut_s = 0;
+        tt_measure_opts mo;
+        scoring_opts(*sp, c->device, *o, inc, &mo);                                            // Z12
         costs->resize(cands.size());
         for (size_t i = 0; i < cands.size(); ++i) {
           tt_sample smp;
@@ -150,6 +150,8 @@ void tt_measure_opts_default(tt_measure_opts* m) {
   m->l2_flush = 0;
   m->max_number = 1000;
   m->graph = 1;
+  m->race_s = 0.0;
+  m->race_repeats = 3;
 }
 
 void tt_search_opts_default(tt_search_opts* o) {
@@ -180,6 +182,9 @@ void tt_search_opts_default(tt_search_opts* o) {
   o->steps_T_floor = 1;
   o->steps_T_decay_every = 0;
   o->layout = TT_LAYOUT_NN;
+  o->train_per_candidate = 0;
+  o->cut_roofline_x = 50.0;
+  o->race_factor = 1.25;
 }
 
 tt_status tt_count_configs(const tt_space* sp, uint64_t* raw, uint64_t* feasible) {
@@ -431,6 +436,51 @@ tt_status tt_measure(tt_ctx* ctx, const tt_space* sp, const tt_config* cfg, cons
 tt_status tt_aggregate(const double* per_repeat, int32_t R, tt_sample* out) {
   if (!per_repeat || !out || R < 1) return fail(TT_E_INVAL, "tt_aggregate needs R >= 1 samples and an output");
   aggregate_repeats(per_repeat, R, out);
+  return TT_OK;
+}
+
+tt_status tt_roofline_seconds(const tt_space* sp, int32_t device, double* seconds) {
+  CHECK_SPACE(sp);
+  if (!seconds) return fail(TT_E_INVAL, "null seconds");
+  *seconds = roofline_seconds(Space(*sp, false), device);
+  return TT_OK;
+}
+
+tt_status tt_scoring_opts(const tt_space* sp, int32_t device, const tt_search_opts* opts, double cost_min,
+                          tt_measure_opts* out) {
+  CHECK_SPACE(sp);
+  if (!opts || !out) return fail(TT_E_INVAL, "null argument");
+  scoring_opts(Space(*sp, false), device, *opts, cost_min, out);
+  return TT_OK;
+}
+
+tt_status tt_measure_set(tt_ctx* ctx, const tt_space* sp, const tt_config* cfgs, int32_t n, const uint8_t* mine,
+                         const tt_measure_opts* mo, double* costs, double* secs) {
+  CHECK_SPACE(sp);
+  if (!ctx || (n > 0 && (!cfgs || !costs)) || n < 0) return fail(TT_E_INVAL, "null argument");
+  if (sp->family == TT_FAM_NONE) return fail(TT_E_UNSUPPORTED, "family NONE has no kernel");
+  tt_measure_opts m;
+  if (mo) m = *mo;
+  else tt_measure_opts_default(&m);
+  Space s(*sp, false);
+  Ctx* c = static_cast<Ctx*>(ctx);
+  for (int32_t j = 0; j < n; ++j) {
+    costs[j] = 0.0;
+    if (secs) secs[j] = 0.0;
+  }
+  for (int32_t j = 0; j < n; ++j) {
+    if (mine && !mine[j]) continue;
+    State st = from_cfg(cfgs[j]);
+    if (!s.j_prod(st)) return fail(TT_E_ILLEGITIMATE, "J_prod false");
+    if (!s.j_hw(st)) return fail(TT_E_INFEASIBLE, "J_hw false");
+    const auto t0 = std::chrono::steady_clock::now();
+    tt_sample smp;
+    std::string err;
+    tt_status r = c->measure(s, st, m, &smp, &err);
+    if (r != TT_OK) return fail(r, err);
+    costs[j] = smp.cost_s;
+    if (secs) secs[j] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
   return TT_OK;
 }
 

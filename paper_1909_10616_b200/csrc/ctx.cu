@@ -99,6 +99,34 @@ void aggregate_repeats(const double* per, int R, tt_sample* out) {
   out->repeats = R;
 }
 
+// ---------------------------------------------------------------- scoring budget (Z12)
+double roofline_seconds(const Space& sp, int device) {
+  int sms = 0, khz = 0;
+  if (device < 0 && cudaGetDevice(&device) != cudaSuccess) device = -1;
+  if (device < 0 || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
+      cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device) != cudaSuccess || sms <= 0 || khz <= 0) {
+    cudaGetLastError();
+    sms = 148;
+    khz = 1965000;
+  }
+  const double fpc = sp.family == TT_FAM_BF16_UMMA ? 8192.0 : (sp.family == TT_FAM_TF32_UMMA ? 4096.0 : 256.0);
+  return 2.0 * (double)sp.dim[0] * (double)sp.dim[1] * (double)sp.dim[2] / ((double)sms * khz * 1e3 * fpc);
+}
+
+void scoring_opts(const Space& sp, int device, const tt_search_opts& o, double cost_min, tt_measure_opts* mo) {
+  *mo = o.measure;
+  if (mo->cut_s == 0) {
+    // probe > cut: scored by its one probe.  Relative part: 20 x the incumbent (never below 1 ms);
+    // absolute part: cut_roofline_x x the roofline time (applies to s0 as well)
+    double cut = std::isfinite(cost_min) ? std::max(20.0 * cost_min, 1e-3) : INFINITY;
+    if (o.cut_roofline_x > 0) cut = std::min(cut, std::max(1e-3, o.cut_roofline_x * roofline_seconds(sp, device)));
+    mo->cut_s = std::isfinite(cut) ? cut : 0.0;
+  }
+  if (mo->cut_s < 0) mo->cut_s = 0;
+  if (mo->race_s == 0 && o.race_factor > 0 && std::isfinite(cost_min)) mo->race_s = o.race_factor * cost_min;
+  if (mo->race_s < 0) mo->race_s = 0;
+}
+
 // ---------------------------------------------------------------- ctx
 
 namespace {
@@ -235,8 +263,10 @@ tt_status Ctx::measure(const Space& sp, const State& s, const tt_measure_opts& m
   const int warm = mo.warmup >= 0 ? mo.warmup : 2;
   for (int w = 0; w < warm; ++w)
     if ((st = launch()) != TT_OK) return st;
-  if ((st = timed_once(&probe)) != TT_OK) return st;   // warm probe sizes `number`
-  out->probe_s = probe;
+  if (!mo.l2_flush) {                                  // a warm probe sizes `number` (1 when flushing)
+    if ((st = timed_once(&probe)) != TT_OK) return st;
+    out->probe_s = probe;
+  }
   float ms = 0;
   const int R = std::max(1, std::min(mo.repeats > 0 ? mo.repeats : 10, kMaxRepeats));
   const double mr = mo.min_repeat_s > 0 ? mo.min_repeat_s : 5e-4;
@@ -279,27 +309,47 @@ tt_status Ctx::measure(const Space& sp, const State& s, const tt_measure_opts& m
       nodes = 0;
     }
   }
-  for (int r = 0; r < R; ++r) {
-    if (mo.l2_flush && (st = flush_l2(err)) != TT_OK) return st;
-    cudaEventRecord(ev[2 + 2 * r], stream);
-    if (ge) {
-      for (int j = 0; j < glaunch; ++j) cudaGraphLaunch(ge, stream);
-    } else {
-      for (int i = 0; i < number; ++i)
-        if ((st = launch()) != TT_OK) return st;
+  auto run_repeats = [&](int r0, int r1) -> tt_status {
+    for (int r = r0; r < r1; ++r) {
+      if (mo.l2_flush && (st = flush_l2(err)) != TT_OK) return st;
+      cudaEventRecord(ev[2 + 2 * r], stream);
+      if (ge) {
+        for (int j = 0; j < glaunch; ++j) cudaGraphLaunch(ge, stream);
+      } else {
+        for (int i = 0; i < number; ++i)
+          if ((st = launch()) != TT_OK) return st;
+      }
+      cudaEventRecord(ev[3 + 2 * r], stream);
     }
-    cudaEventRecord(ev[3 + 2 * r], stream);
-  }
-  const bool synced = cuda_ok(cudaEventSynchronize(ev[1 + 2 * R]), err, "measure");
-  if (ge) cudaGraphExecDestroy(ge);
-  if (!synced) return TT_E_CUDA;
+    return cuda_ok(cudaEventSynchronize(ev[1 + 2 * r1]), err, "measure") ? TT_OK : TT_E_CUDA;
+  };
   std::vector<double> per(R);
-  for (int r = 0; r < R; ++r) {
-    cudaEventElapsedTime(&ms, ev[2 + 2 * r], ev[3 + 2 * r]);
-    per[r] = ms * 1e-3 / number;
+  auto collect = [&](int r0, int r1) {
+    for (int r = r0; r < r1; ++r) {
+      cudaEventElapsedTime(&ms, ev[2 + 2 * r], ev[3 + 2 * r]);
+      per[r] = ms * 1e-3 / number;
+    }
+  };
+  // Racing (reading Z12): a candidate whose first race_repeats repeats all exceed race_s (a margin
+  // over the incumbent) cannot become the best; it is scored by those repeats alone.
+  const int rr = mo.race_s > 0 ? std::max(1, mo.race_repeats > 0 ? mo.race_repeats : 3) : R;
+  int done = std::min(rr, R);
+  st = run_repeats(0, done);
+  if (st == TT_OK) {
+    collect(0, done);
+    const bool lost = mo.race_s > 0 && done < R && *std::min_element(per.begin(), per.begin() + done) > mo.race_s;
+    if (lost) {
+      out->raced = 1;
+    } else if (done < R) {
+      st = run_repeats(done, R);
+      if (st == TT_OK) collect(done, R);
+      done = R;
+    }
   }
-  aggregate_repeats(per.data(), R, out);
-  out->repeats = R;
+  if (ge) cudaGraphExecDestroy(ge);
+  if (st != TT_OK) return st;
+  const int R_run = out->raced ? done : R;
+  aggregate_repeats(per.data(), R_run, out);
   out->number = number;
   out->graph_nodes = nodes;
   return cuda_ok(cudaGetLastError(), err, "measure") ? TT_OK : TT_E_CUDA;

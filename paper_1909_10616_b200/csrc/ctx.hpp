@@ -18,6 +18,11 @@ constexpr int kGraphNodes = 32;   // launches captured per measurement graph
 // cost = median of the R per-repeat means; mean / min / stdev beside it (reading Z10, tt_aggregate)
 void aggregate_repeats(const double* per, int R, tt_sample* out);
 
+// 2MNK at the family's nominal peak on `device` (-1 = current; 148 SMs x 1965 MHz without one)
+double roofline_seconds(const Space& sp, int device);
+// per-candidate measurement options of a search at incumbent cost_min (reading Z12)
+void scoring_opts(const Space& sp, int device, const tt_search_opts& o, double cost_min, tt_measure_opts* mo);
+
 struct Operands {
   int64_t M = 0, N = 0, K = 0;
   int dtype = 0;  // 0 fp32, 1 bf16

@@ -4,84 +4,164 @@ Two partitions of the hot path:
 
 1. Candidate-batch sharding for the searches.  Every rank runs the identical search (same
    seed, same code, replicated state); a round's candidates are independent measurements, so
-   candidate j is measured on rank j mod G and the (j, cost) pairs are all-gathered.  The
-   traversal depends only on (seed, W, rho, cost values), never on G.
+   each is measured on exactly one rank and the costs are exchanged.  The traversal depends only
+   on (seed, W, rho, cost values), never on G or on which rank measured what.
 2. Row-partitioned large GEMM: rank r owns rows [r M/G, (r+1) M/G) of A and C, B is
    replicated, and there is no collective on the math path (``row_shard``).
 
 torch is used for the process group and the tiny timing tensors only; every measurement is a
-libtiletune call.
+libtiletune call (``tt_measure_set``: the per-rank half of a round runs in C++, one call per round).
 """
 from __future__ import annotations
 
+import itertools
 import math
 import time
-from typing import Callable, List, Optional, Sequence
+from typing import Callable, List, Optional, Sequence, Tuple
 
 import torch
 import torch.distributed as dist
 
 from . import tiletune as tt
 
+# measurement-time model of one candidate for the LPT assignment: a candidate scored by its
+# probe costs one launch, a full one ~13 (cold probe, 2 warmups, 10 repeats), plus host overhead
+_FULL_LAUNCHES = 13
+_PER_CANDIDATE_S = 2e-3
+
 
 class ShardedEvaluator:
-    """BATCH cost source for tt.gbfs_search / tt.na2c_search.
+    """BATCH cost source for tt.gbfs_search / tt.na2c_search / tt.random_search.
 
-    ``measure_one(state) -> float`` scores one candidate on this rank (normally a
-    ``tt.Context.measure``).  Assignment of a round's candidates to ranks:
+    ``measure_set(states, mine) -> (costs, seconds)`` scores the states whose ``mine`` flag is
+    set on this rank (normally ``device_measure_set``: one tt_measure_set call, C++ loop) and
+    returns 0 elsewhere.  For host-side tests ``measure_one(state) -> cost`` is accepted instead.
 
-    * static (default): candidate j on rank j mod G; one all_gather of a [G, n] float64 tensor;
-    * dynamic (``store`` given): ranks claim the next unmeasured candidate index from a shared
-      counter (``store.add``, the process group's TCPStore) as soon as they are free, so one slow
-      candidate does not hold up the others; one all_reduce(MAX) of an [n] float64 tensor whose
-      entries only the claiming rank filled (costs are > 0).
+    Assignment of a round's candidates to ranks (``assign``):
 
-    Either way each candidate is measured exactly once and the costs are returned by index, so
-    the traversal depends only on (seed, W, rho, costs), never on G or on the assignment.
+    * ``"lpt"`` (default): longest predicted measurement first, each to the least-loaded rank.
+      The prediction of a candidate is the lowest known cost among its measured neighbours (a
+      neighbour differs by one x2 / /2 move), turned into a measurement time by the
+      scoring rules (one launch above the cut, ~13 below).  Every rank holds the same known
+      costs, so every rank computes the same assignment with no communication.
+    * ``"static"``: candidate j on rank j mod G.
+    * ``"dynamic"`` (``store`` given): ranks claim the next unmeasured index from a shared
+      counter (``store.add``) whenever they are free.
+
+    Costs are exchanged with one all_reduce(MAX) of an [n] float64 vector whose entries only the
+    measuring rank filled (every cost is > 0), so each candidate is measured exactly once and the
+    costs come back by index.
     """
 
-    def __init__(self, measure_one: Callable, group=None, device: Optional[torch.device] = None, store=None):
-        self.measure_one = measure_one
+    _instances = itertools.count()     # per-process: identical on every rank that builds evaluators in order
+
+    def __init__(self, measure_one: Optional[Callable] = None, group=None, device: Optional[torch.device] = None,
+                 store=None, measure_set: Optional[Callable] = None, assign: Optional[str] = None,
+                 space: Optional[tt.Space] = None, cut_s: Optional[Callable[[], float]] = None):
+        if measure_set is None:
+            if measure_one is None:
+                raise ValueError("need measure_one or measure_set")
+
+            def measure_set(states, mine):
+                costs, secs = [0.0] * len(states), [0.0] * len(states)
+                for j, (s, m) in enumerate(zip(states, mine)):
+                    if m:
+                        t0 = time.perf_counter()
+                        costs[j] = float(measure_one(s))
+                        secs[j] = time.perf_counter() - t0
+                return costs, secs
+        self.measure_set = measure_set
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.device = device or torch.device("cpu")
         self.store = store if self.world > 1 else None
+        self.assign = "dynamic" if self.store is not None else (assign or "lpt")
+        if self.assign == "dynamic" and self.store is None and self.world > 1:
+            raise ValueError("dynamic assignment needs a store")
+        self.space = space
+        self.cut_s = cut_s
+        self.ns = f"tt_eval{next(ShardedEvaluator._instances)}"
         self.rounds = 0
         self.local_evals = 0
-        self.round_times: List[List[float]] = []   # per round: wall time of each local measurement
+        self.known: dict = {}
+        # per round: (measurement seconds of every candidate on the rank that measured it -- the
+        # values are exchanged with the costs --, predicted weights used by the LPT assignment)
+        self.round_times: List[List[float]] = []
+        self.round_weights: List[List[float]] = []
 
-    def _measure(self, states, j, mine, times):
-        t0 = time.perf_counter()
-        mine[j] = float(self.measure_one(states[j]))
-        times[j] = time.perf_counter() - t0
-        self.local_evals += 1
+    # ------------------------------------------------------------------ assignment
+    def _predicted_cost(self, s) -> float:
+        best = math.inf
+        if self.space is not None:
+            for t in tt.neighbors(self.space, s):
+                c = self.known.get(t)
+                if c is not None and c < best:
+                    best = c
+        if not math.isfinite(best):
+            best = min(self.known.values()) if self.known else 1.0
+        return best
 
+    def weights(self, states) -> List[float]:
+        cut = self.cut_s() if self.cut_s is not None else 0.0
+        w = []
+        for s in states:
+            c = self._predicted_cost(s)
+            w.append((c if (cut > 0 and c > cut) else _FULL_LAUNCHES * c) + _PER_CANDIDATE_S)
+        return w
+
+    @staticmethod
+    def lpt_owners(weights: Sequence[float], world: int) -> List[int]:
+        """Longest-processing-time-first list scheduling: candidates in decreasing weight (ties by
+        index) go to the least-loaded rank (ties: lowest rank).  Deterministic."""
+        owner = [0] * len(weights)
+        load = [0.0] * world
+        for j in sorted(range(len(weights)), key=lambda j: (-weights[j], j)):
+            r = min(range(world), key=lambda i: (load[i], i))
+            owner[j] = r
+            load[r] += weights[j]
+        return owner
+
+    # ------------------------------------------------------------------ one round
     def __call__(self, states: Sequence) -> List[float]:
         n = len(states)
-        mine = torch.zeros(n, dtype=torch.float64, device=self.device)
-        times = [0.0] * n
-        if self.store is not None:
-            key = f"tt_round_{self.rounds}"
+        wts = self.weights(states) if self.assign == "lpt" else [1.0] * n
+        vals = torch.zeros(2 * n, dtype=torch.float64, device=self.device)   # costs, then seconds
+        if self.assign == "dynamic":
+            key = f"{self.ns}_round{self.rounds}"
             while True:
                 j = int(self.store.add(key, 1)) - 1
                 if j >= n:
                     break
-                self._measure(states, j, mine, times)
+                mine = [i == j for i in range(n)]
+                c, t = self.measure_set(states, mine)
+                vals[j], vals[n + j] = c[j], t[j]
+                self.local_evals += 1
         else:
-            for j in range(self.rank, n, self.world):
-                self._measure(states, j, mine, times)
-        self.round_times.append(times)
+            owner = self.lpt_owners(wts, self.world) if self.assign == "lpt" else [j % self.world for j in range(n)]
+            mine = [o == self.rank for o in owner]
+            c, t = self.measure_set(states, mine)
+            for j in range(n):
+                if mine[j]:
+                    vals[j], vals[n + j] = c[j], t[j]
+                    self.local_evals += 1
+        if self.world > 1:
+            dist.all_reduce(vals, op=dist.ReduceOp.MAX, group=self.group)
+            if self.assign == "dynamic" and self.rank == 0:
+                try:                                     # every rank has left its claim loop
+                    self.store.delete_key(f"{self.ns}_round{self.rounds}")
+                except Exception:  # noqa: BLE001 - older stores: keys are namespaced anyway
+                    pass
+        out = vals.cpu().tolist()
+        costs = out[:n]
+        if not all(c > 0 for c in costs):
+            raise RuntimeError(f"sharded round {self.rounds}: a candidate came back unmeasured ({costs})")
+        self.round_times.append(out[n:])
+        self.round_weights.append(wts)
         self.rounds += 1
-        if self.world == 1:
-            return mine.tolist()
-        if self.store is not None:
-            dist.all_reduce(mine, op=dist.ReduceOp.MAX, group=self.group)
-            return [float(x) for x in mine.cpu().tolist()]
-        out = torch.empty(self.world * n, dtype=torch.float64, device=self.device)
-        dist.all_gather_into_tensor(out, mine, group=self.group)
-        g = out.view(self.world, n).cpu()
-        return [float(g[j % self.world, j]) for j in range(n)]
+        for s, c in zip(states, costs):
+            self.known[s] = c
+        return costs
 
 
 def default_store():
@@ -93,60 +173,67 @@ def default_store():
         return None
 
 
-def device_measure(ctx: tt.Context, sp: tt.Space, opts: Optional[tt.MeasureOpts] = None, cut_factor: float = 20.0,
-                   cut_floor_s: float = 0.05):
-    """measure_one for ShardedEvaluator: tt_measure with the slow-candidate cut of reading Z12
-    driven by the best cost seen so far (identical on every rank: it is computed from the
-    gathered costs the search pushes)."""
+def device_measure_set(ctx: tt.Context, sp: tt.Space, opts: tt.SearchOpts, device: int = -1):
+    """measure_set for ShardedEvaluator on the device: one tt_measure_set call per round with the
+    search's scoring options (tt_scoring_opts: slow-candidate cut and racing, reading Z12) at the
+    incumbent -- identical on every rank, because it is the minimum of the exchanged costs.
+    Returns (measure_set, observe, cut_s) where observe(costs) updates the incumbent and cut_s()
+    is the current cut (for the LPT weights)."""
     state = {"best": math.inf}
-    base = opts or tt.measure_opts()
 
-    def f(s):
-        mo = tt.MeasureOpts.from_buffer_copy(base)
-        if math.isfinite(state["best"]):
-            mo.cut_s = max(cut_factor * state["best"], cut_floor_s)
-        c = ctx.measure(sp, s, mo).cost_s
-        return c
+    def mo():
+        return tt.scoring_opts(sp, opts, state["best"], device)
+
+    def measure_set(states, mine):
+        return ctx.measure_set(sp, states, mine, mo())
 
     def observe(costs):
         for c in costs:
             state["best"] = min(state["best"], c)
 
-    return f, observe
+    return measure_set, observe, lambda: mo().cut_s
 
 
 def projected_sharded_wall(round_times: Sequence[Sequence[float]], world: int, per_round_s: float = 0.0,
-                           dynamic: bool = False, per_claim_s: float = 0.0) -> float:
+                           dynamic: bool = False, per_claim_s: float = 0.0,
+                           weights: Optional[Sequence[Sequence[float]]] = None) -> float:
     """Measurement wall time of the same traversal sharded over ``world`` ranks, from
     per-candidate times recorded on one rank: sum over rounds of the slowest rank's busy time,
     plus ``per_round_s`` (the collective) per round.  Static: candidate j on rank j mod world.
+    ``weights`` given: the LPT assignment the evaluator makes from those predicted weights.
     Dynamic: candidates in index order each go to the rank that becomes free first (what the
     counter-claiming evaluator does), each claim costing ``per_claim_s``.  A projection from
     measured times, not a multi-GPU measurement."""
     total = 0.0
-    for times in round_times:
+    for k, times in enumerate(round_times):
         busy = [0.0] * world
+        if weights is not None:
+            owner = ShardedEvaluator.lpt_owners(weights[k], world)
         for j, t in enumerate(times):
-            r = min(range(world), key=lambda i: busy[i]) if dynamic else j % world
+            if weights is not None:
+                r = owner[j]
+            else:
+                r = min(range(world), key=lambda i: busy[i]) if dynamic else j % world
             busy[r] += t + (per_claim_s if dynamic else 0.0)
         total += max(busy) + (per_round_s if world > 1 else 0.0)
     return total
 
 
 class TrackingEvaluator(ShardedEvaluator):
-    """ShardedEvaluator that feeds the gathered costs back into a cut tracker."""
+    """ShardedEvaluator that feeds the exchanged costs back into the scoring tracker."""
 
-    def __init__(self, measure_one, observe, **kw):
+    def __init__(self, measure_one=None, observe=None, **kw):
         super().__init__(measure_one, **kw)
         self.observe = observe
 
     def __call__(self, states):
         costs = super().__call__(states)
-        self.observe(costs)
+        if self.observe is not None:
+            self.observe(costs)
         return costs
 
 
-def row_shard(M: int, world: int, rank: int):
+def row_shard(M: int, world: int, rank: int) -> Tuple[int, int]:
     """Rows [r0, r1) of the row-partitioned GEMM owned by ``rank`` (exact: M % world == 0)."""
     if M % world:
         raise ValueError("row partition needs M divisible by the number of ranks")

@@ -37,12 +37,13 @@ class Config(C.Structure):
 class Sample(C.Structure):
     _fields_ = [("cost_s", dbl), ("mean_s", dbl), ("min_s", dbl), ("stdev_s", dbl), ("probe_s", dbl),
                 ("repeats", i32), ("number", i32), ("device", i32), ("slow_cut", i32), ("graph_nodes", i32),
-                ("reserved", i32)]
+                ("raced", i32)]
 
 
 class MeasureOpts(C.Structure):
     _fields_ = [("warmup", i32), ("repeats", i32), ("min_repeat_s", dbl), ("cut_s", dbl), ("l2_flush", i32),
-                ("max_number", i32), ("graph", i32)]
+                ("max_number", i32), ("graph", i32),
+                ("race_s", dbl), ("race_repeats", i32)]
 
 
 class TraceRow(C.Structure):
@@ -67,7 +68,7 @@ class SearchOpts(C.Structure):
                 ("batch", i32), ("mem_capacity", i32), ("gamma", dbl), ("beta", dbl), ("lr", dbl), ("clip", dbl),
                 ("epochs", i32), ("minibatch", i32), ("hidden", i32), ("rollout_cap_factor", i32),
                 ("max_t_increase", i32), ("steps_T_floor", i32), ("steps_T_decay_every", i32), ("layout", i32),
-                ("train_per_candidate", i32)]
+                ("train_per_candidate", i32), ("cut_roofline_x", dbl), ("race_factor", dbl)]
 
 
 class LaunchInfo(C.Structure):
@@ -100,6 +101,10 @@ EXPORTS = {
     "tt_ctx_stream": (i32, [vp, C.POINTER(vp)]),
     "tt_ctx_operands": (i32, [vp, i64, i64, i64, i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
     "tt_aggregate": (i32, [C.POINTER(dbl), i32, C.POINTER(Sample)]),
+    "tt_roofline_seconds": (i32, [C.POINTER(Space), i32, C.POINTER(dbl)]),
+    "tt_scoring_opts": (i32, [C.POINTER(Space), i32, C.POINTER(SearchOpts), dbl, C.POINTER(MeasureOpts)]),
+    "tt_measure_set": (i32, [vp, C.POINTER(Space), C.POINTER(Config), i32, C.POINTER(C.c_uint8),
+                             C.POINTER(MeasureOpts), C.POINTER(dbl), C.POINTER(dbl)]),
     "tt_measure": (i32, [vp, C.POINTER(Space), C.POINTER(Config), C.POINTER(MeasureOpts), C.POINTER(Sample)]),
     "tt_gbfs_search": (i32, [vp, i64, i64, i64, u64, C.POINTER(SearchOpts), C.POINTER(Result),
                              C.POINTER(TraceRow), u64]),
@@ -303,6 +308,20 @@ def aggregate(per_repeat: Sequence[float]) -> Sample:
     return out
 
 
+def roofline_seconds(sp: Space, device: int = -1) -> float:
+    """One GEMM of sp at the family's nominal device peak (tt_roofline_seconds)."""
+    t = dbl()
+    _check(lib.tt_roofline_seconds(C.byref(sp), device, C.byref(t)), "roofline_seconds")
+    return t.value
+
+
+def scoring_opts(sp: Space, opts: "SearchOpts", cost_min: float, device: int = -1) -> "MeasureOpts":
+    """Per-candidate measurement options of a search at incumbent cost_min (tt_scoring_opts, Z12)."""
+    mo = MeasureOpts()
+    _check(lib.tt_scoring_opts(C.byref(sp), device, C.byref(opts), cost_min, C.byref(mo)), "scoring_opts")
+    return mo
+
+
 def measure_opts(**kw) -> MeasureOpts:
     mo = MeasureOpts()
     lib.tt_measure_opts_default(C.byref(mo))
@@ -345,6 +364,18 @@ class Context:
         _check(lib.tt_measure(self.h, C.byref(sp), C.byref(to_config(s)), C.byref(opts) if opts else None,
                               C.byref(out)), "measure")
         return out
+
+    def measure_set(self, sp: Space, states: Sequence[State], mine: Optional[Sequence[bool]] = None,
+                    opts: Optional[MeasureOpts] = None):
+        """tt_measure_set: costs (and host seconds) of the states with mine[j] true, 0 elsewhere."""
+        n = len(states)
+        cfgs = (Config * max(n, 1))(*[to_config(s) for s in states])
+        mk = (C.c_uint8 * max(n, 1))(*[1 if m else 0 for m in mine]) if mine is not None else None
+        costs = (dbl * max(n, 1))()
+        secs = (dbl * max(n, 1))()
+        _check(lib.tt_measure_set(self.h, C.byref(sp), cfgs, n, mk, C.byref(opts) if opts else None, costs, secs),
+               "measure_set")
+        return [costs[j] for j in range(n)], [secs[j] for j in range(n)]
 
     def gemm_host(self, A_host, B_host, C_host, family: int, s: State, layout: int = LAYOUT_NN):
         M, N, K = _check_gemm_operands(A_host, B_host, C_host, family, layout, on_device=False)

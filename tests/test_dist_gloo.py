@@ -20,7 +20,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, algo, out, dynamic=False):
+def _worker(rank, world, port, algo, out, mode="static"):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -36,23 +36,34 @@ def _worker(rank, world, port, algo, out, dynamic=False):
         measured.append(s)
         return costs.t2_cost(sp, s)
 
-    ev = tdist.ShardedEvaluator(measure_one, store=tdist.default_store() if dynamic else None)
-    assert (ev.store is not None) == dynamic
+    def make():
+        return tdist.ShardedEvaluator(measure_one, store=tdist.default_store() if mode == "dynamic" else None,
+                                      assign=mode if mode != "dynamic" else None,
+                                      space=tt.make_space(64, 64, 64) if mode == "lpt" else None)
+
+    ev = make()
+    assert ev.assign == mode
     if algo == "gbfs":
         res = tt.gbfs_search(64, 64, 64, 300, tt.search_opts(seed=4, width=8), batch=ev)
     else:
         res = tt.na2c_search(64, 64, 64, 200, tt.search_opts(seed=4, epsilon=0.0), batch=ev)
+    # a second search in the same process group (fresh evaluator: its own store keys)
+    n_first = len(measured)
+    ev2 = make()
+    res2 = tt.gbfs_search(64, 64, 64, 120, tt.search_opts(seed=9, width=4), batch=ev2)
     row_ranges = tdist.row_shard(8192, world, rank)
-    out[rank] = ([(r["state"], r["cost"]) for r in res.trace], len(measured), ev.rounds, row_ranges)
+    out[rank] = ([(r["state"], r["cost"]) for r in res.trace], n_first, ev.rounds, row_ranges,
+                 [(r["state"], r["cost"]) for r in res2.trace], len(measured) - n_first)
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("algo,dynamic", [("gbfs", False), ("na2c", False), ("gbfs", True), ("na2c", True)])
-def test_sharded_search_matches_oracle(algo, dynamic):
+@pytest.mark.parametrize("algo,mode", [("gbfs", "static"), ("na2c", "static"), ("gbfs", "dynamic"),
+                                       ("na2c", "dynamic"), ("gbfs", "lpt"), ("na2c", "lpt")])
+def test_sharded_search_matches_oracle(algo, mode):
     world = 2
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), algo, out, dynamic), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), algo, out, mode), nprocs=world, join=True)
     sp = Spec(64, 64, 64)
     tab = costs.table(sp, lambda s: costs.t2_cost(sp, s))
     if algo == "gbfs":
@@ -60,13 +71,24 @@ def test_sharded_search_matches_oracle(algo, dynamic):
     else:
         o = ona2c.na2c(sp, ogbfs.table_source(sp, tab), budget=200, params=ona2c.Params(epsilon=0.0), seed=4)
     ref = [(r.state, r.cost) for r in o.trace]
-    t0, n0, rounds0, rr0 = out[0]
-    t1, n1, rounds1, rr1 = out[1]
+    t0, n0, rounds0, rr0, u0, m0 = out[0]
+    t1, n1, rounds1, rr1, u1, m1 = out[1]
     assert t0 == t1 == ref                                 # identical traversal on every rank = oracle
     assert n0 + n1 == len(ref)                             # each candidate measured exactly once
-    if not dynamic:
+    if mode == "static":
         assert abs(n0 - n1) <= rounds0                     # round-robin balance
     assert rr0 == (0, 4096) and rr1 == (4096, 8192)        # exact row partition
+    # second search in the same group: still the oracle traversal, each candidate measured once
+    o2 = ogbfs.gbfs(sp, ogbfs.table_source(sp, tab), budget=120, rho=5, seed=9, width=4)
+    assert u0 == u1 == [(r.state, r.cost) for r in o2.trace]
+    assert m0 + m1 == 120
+
+
+def test_lpt_owners():
+    # longest first to the least-loaded rank; deterministic ties
+    assert tdist.ShardedEvaluator.lpt_owners([1.0, 1.0, 1.0, 1.0], 2) == [0, 1, 0, 1]
+    assert tdist.ShardedEvaluator.lpt_owners([5.0, 1.0, 1.0, 1.0, 1.0, 1.0], 2) == [0, 1, 1, 1, 1, 1]
+    assert tdist.ShardedEvaluator.lpt_owners([3.0, 3.0, 2.0, 2.0, 2.0], 2) == [0, 1, 0, 1, 0]
 
 def test_projection():
     rt = [[1.0], [1.0, 2.0, 3.0, 4.0], [0.5] * 8]
@@ -77,3 +99,5 @@ def test_projection():
     # dynamic: list scheduling in index order, each candidate to the first free rank
     assert tdist.projected_sharded_wall([[4.0, 1.0, 1.0, 1.0, 1.0]], 2, dynamic=True) == 4.0
     assert tdist.projected_sharded_wall([[4.0, 1.0, 1.0, 1.0, 1.0]], 2) == 6.0
+    # LPT from predicted weights: the long candidate alone on one rank
+    assert tdist.projected_sharded_wall([[4.0, 1.0, 1.0, 1.0, 1.0]], 2, weights=[[4.0, 1.0, 1.0, 1.0, 1.0]]) == 4.0

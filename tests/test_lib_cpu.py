@@ -367,3 +367,27 @@ def test_binding_rejects_bad_operands():
         tt.Context.gemm_host(ctx, A, torch.zeros(16, 64), C, tt.FAM_F32_SIMT, cfg)
     with pytest.raises(TypeError):
         tt.Context.gemm_host(ctx, A.double(), B, C, tt.FAM_F32_SIMT, cfg)
+
+
+def test_scoring_opts_reading_z12():
+    # reading Z12 (slow candidates) and racing: the options every DEVICE / sharded search uses
+    sp = tt.make_space(2048, 2048, 2048, family=tt.FAM_F32_SIMT)
+    t_roof = tt.roofline_seconds(sp, device=-1)
+    import torch
+    if not torch.cuda.is_available():                 # no device: 148 SMs x 1965 MHz x 256 flop/clk/SM
+        assert t_roof == pytest.approx(2 * 2048 ** 3 / (148 * 1965e6 * 256), rel=1e-12)
+    o = tt.search_opts(family=1)
+    s0 = tt.scoring_opts(sp, o, math.inf)
+    assert s0.cut_s == pytest.approx(max(1e-3, 50 * t_roof)) and s0.race_s == 0.0   # applies to s0 too
+    inc = 385e-6
+    m = tt.scoring_opts(sp, o, inc)
+    assert m.cut_s == pytest.approx(min(max(20 * inc, 1e-3), max(1e-3, 50 * t_roof)))
+    assert m.race_s == pytest.approx(1.25 * inc)
+    big = tt.scoring_opts(sp, o, 5.0)                  # an incumbent near s0: the absolute cut rules
+    assert big.cut_s == pytest.approx(max(1e-3, 50 * t_roof))
+    off = tt.scoring_opts(sp, tt.search_opts(family=1, cut_roofline_x=0.0, race_factor=0.0), math.inf)
+    assert off.cut_s == 0.0 and off.race_s == 0.0
+    fixed = tt.scoring_opts(sp, tt.search_opts(family=1, measure={"cut_s": 0.5}), inc)
+    assert fixed.cut_s == 0.5                          # an explicit cut is kept
+    bf = tt.make_space(4096, 4096, 4096, family=tt.FAM_BF16_UMMA)
+    assert tt.roofline_seconds(bf) < tt.roofline_seconds(tt.make_space(4096, 4096, 4096, family=tt.FAM_F32_SIMT)) / 16
