@@ -252,8 +252,14 @@ def tune(ctx, sp, Mr, N, K, fam, layout, budget, args, world, coll, local):
            "best_cost_us": res.best_cost * 1e6, "s0_cost_us": res.trace[0]["cost"] * 1e6,
            "local_evals": ev.local_evals, "rounds": ev.rounds,
            "scoring": ("L2 flushed before every timed launch" if args.tune_l2_flush else "warm L2, CUDA-graph replay")
-           + "; slow cut min(max(20 cost_min, 1 ms), 50 t_roof), racing at 1.25 cost_min (reading Z12)",
+           + "; slow cut min(max(20 cost_min, 1 ms), 50 t_roof), racing at 1.1 cost_min after 2 repeats (reading Z12)",
            "assignment": ev.assign}
+    if getattr(args, "dump_tuning", None) and (not dist.is_initialized() or dist.get_rank() == 0):
+        with open(args.dump_tuning + f".{sp.family}_{Mr}.jsonl", "w") as f:
+            for k, (ts, ws) in enumerate(zip(ev.round_times, ev.round_weights)):
+                f.write(json.dumps({"round": k, "secs": ts, "weights": ws}) + "\n")
+            for r in res.trace:
+                f.write(json.dumps({"state": r["state"], "cost": r["cost"], "t": r["t_wall_s"]}) + "\n")
     if world == 1:
         # Projection of the sharded search from this run's per-candidate
         # measurement times: each round's candidates assigned by rule, the slowest rank gates the
@@ -400,6 +406,7 @@ def main():
                     help="workload of the fp32 (paper arithmetic) record")
     ap.add_argument("--no-fp32", action="store_true", help="skip the fp32 record")
     ap.add_argument("--config", default=None, help="skip tuning and use this config (JSON triple)")
+    ap.add_argument("--dump-tuning", default=None, help="write per-round / per-candidate tuning data to PATH.*.jsonl")
     ap.add_argument("--tune-warm", dest="tune_l2_flush", action="store_false",
                     help="score candidates warm (CUDA-graph replay) instead of with the timed region's L2 flush")
     args = ap.parse_args()

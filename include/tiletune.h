@@ -87,7 +87,8 @@ typedef struct {
 } tt_sample;
 
 typedef struct {
-  int32_t warmup;          /* untimed launches before the probe (default 2) */
+  int32_t warmup;          /* untimed launches between the cold probe and the repeats (default 2;
+                              none with l2_flush, where every timed launch starts cold) */
   int32_t repeats;         /* R (default 10) */
   double min_repeat_s;     /* each repeat lasts >= this: number = ceil(min_repeat_s / probe) (5e-4) */
   double cut_s;            /* if > 0 and probe > cut_s: cost = probe, repeats = 1 (Z12) */
@@ -99,7 +100,7 @@ typedef struct {
   double race_s;           /* if > 0: when the first race_repeats repeats all exceed race_s, stop
                               there (cost = their median, raced = 1) -- a candidate that cannot
                               beat the incumbent is not timed to full precision (reading Z12) */
-  int32_t race_repeats;    /* default 3 */
+  int32_t race_repeats;    /* default 2 */
 } tt_measure_opts;
 
 /* One row per measured state, in evaluation order (Fig. 7 axes P:352). */
@@ -172,7 +173,7 @@ typedef struct {
   /* Scoring budget of the DEVICE / batch cost sources (reading Z12, "searching time" P:359):
    * cut_s = min(max(20 cost_min, 1 ms), max(1 ms, cut_roofline_x t_roof)), applied from s0 on
    * (t_roof = tt_roofline_seconds), and race_s = race_factor cost_min.  cut_roofline_x <= 0 drops the
-   * absolute cut; race_factor <= 0 disables racing.  Defaults 50 and 1.25. */
+   * absolute cut; race_factor <= 0 disables racing.  Defaults 50 and 1.1. */
   double cut_roofline_x;
   double race_factor;
 } tt_search_opts;

@@ -151,7 +151,7 @@ void tt_measure_opts_default(tt_measure_opts* m) {
   m->max_number = 1000;
   m->graph = 1;
   m->race_s = 0.0;
-  m->race_repeats = 3;
+  m->race_repeats = 2;
 }
 
 void tt_search_opts_default(tt_search_opts* o) {
@@ -184,7 +184,7 @@ void tt_search_opts_default(tt_search_opts* o) {
   o->layout = TT_LAYOUT_NN;
   o->train_per_candidate = 0;
   o->cut_roofline_x = 50.0;
-  o->race_factor = 1.25;
+  o->race_factor = 1.1;
 }
 
 tt_status tt_count_configs(const tt_space* sp, uint64_t* raw, uint64_t* feasible) {

@@ -260,7 +260,9 @@ tt_status Ctx::measure(const Space& sp, const State& s, const tt_measure_opts& m
     out->slow_cut = 1;
     return TT_OK;
   }
-  const int warm = mo.warmup >= 0 ? mo.warmup : 2;
+  // warm-up launches only matter when the repeats run warm: under the L2 flush every timed launch
+  // starts cold (reading Z11), and the cold probe has already run the config once
+  const int warm = mo.l2_flush ? 0 : (mo.warmup >= 0 ? mo.warmup : 2);
   for (int w = 0; w < warm; ++w)
     if ((st = launch()) != TT_OK) return st;
   if (!mo.l2_flush) {                                  // a warm probe sizes `number` (1 when flushing)
@@ -332,7 +334,7 @@ tt_status Ctx::measure(const Space& sp, const State& s, const tt_measure_opts& m
   };
   // Racing (reading Z12): a candidate whose first race_repeats repeats all exceed race_s (a margin
   // over the incumbent) cannot become the best; it is scored by those repeats alone.
-  const int rr = mo.race_s > 0 ? std::max(1, mo.race_repeats > 0 ? mo.race_repeats : 3) : R;
+  const int rr = mo.race_s > 0 ? std::max(1, mo.race_repeats > 0 ? mo.race_repeats : 2) : R;
   int done = std::min(rr, R);
   st = run_repeats(0, done);
   if (st == TT_OK) {

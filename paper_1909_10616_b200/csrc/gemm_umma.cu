@@ -771,7 +771,7 @@ constexpr int kMaxPieces = 4;
 int tail_split_mode() {
   const char* e = std::getenv("TT_TAIL_SPLIT");
   if (!e || !e[0]) return 1;
-  return e[0] == '0' ? 0 : (e[0] == '2' ? 2 : 1);
+  return (e[0] >= '0' && e[0] <= '4') ? e[0] - '0' : 1;
 }
 
 template <int KIND, int CG>
@@ -925,7 +925,19 @@ void plan_of(const Space& sp, const State& s, Plan* pl) {
   const double gain_us = (1.0 - (double)rem / P) * tile_us;
   const int mode = tail_split_mode();
   const bool worth = tiles - rem >= P && a.acc_bufs == 2 && gain_us >= 8.0;
-  if (mode != 0 && rem != 0 && a.k0 >= 2 && (mode == 2 || worth)) {
+  if (mode == 3 && a.k0 >= 2 && tiles * pl->csize <= kFlagWords) {
+    // experiment: stream-K over every tile (each cluster gets tiles k0 / P k-blocks)
+    a.sk_tiles = tiles;
+    a.dp_tiles = 0;
+    a.sk_workers = P;
+    pl->grid = P * pl->csize;
+  } else if (mode == 4 && rem != 0 && a.k0 >= 2 && tiles >= rem + P && (rem + P) * pl->csize <= kFlagWords) {
+    // experiment: data-parallel waves, then the last full wave plus the remainder by stream-K
+    a.sk_tiles = rem + P;
+    a.dp_tiles = tiles - a.sk_tiles;
+    a.sk_workers = P;
+    pl->grid = P * pl->csize;
+  } else if (mode != 0 && mode < 3 && rem != 0 && a.k0 >= 2 && (mode == 2 || worth)) {
     a.sk_tiles = tiles % P;                              // == tiles when tiles < P
     a.dp_tiles = tiles - a.sk_tiles;
     a.sk_workers = std::min(P, a.sk_tiles * kMaxPieces);

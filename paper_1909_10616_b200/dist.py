@@ -25,8 +25,8 @@ import torch.distributed as dist
 from . import tiletune as tt
 
 # measurement-time model of one candidate for the LPT assignment: a candidate scored by its
-# probe costs one launch, a full one ~13 (cold probe, 2 warmups, 10 repeats), plus host overhead
-_FULL_LAUNCHES = 13
+# probe costs one launch, a full one ~11 (cold probe, 10 repeats), plus host overhead
+_FULL_LAUNCHES = 11
 _PER_CANDIDATE_S = 2e-3
 
 
@@ -42,7 +42,7 @@ class ShardedEvaluator:
     * ``"lpt"`` (default): longest predicted measurement first, each to the least-loaded rank.
       The prediction of a candidate is the lowest known cost among its measured neighbours (a
       neighbour differs by one x2 / /2 move), turned into a measurement time by the
-      scoring rules (one launch above the cut, ~13 below).  Every rank holds the same known
+      scoring rules (one launch above the cut, ~11 below).  Every rank holds the same known
       costs, so every rank computes the same assignment with no communication.
     * ``"static"``: candidate j on rank j mod G.
     * ``"dynamic"`` (``store`` given): ranks claim the next unmeasured index from a shared
@@ -85,16 +85,23 @@ class ShardedEvaluator:
         self.rounds = 0
         self.local_evals = 0
         self.known: dict = {}
+        self._nb_cache: dict = {}
         # per round: (measurement seconds of every candidate on the rank that measured it -- the
         # values are exchanged with the costs --, predicted weights used by the LPT assignment)
         self.round_times: List[List[float]] = []
         self.round_weights: List[List[float]] = []
 
     # ------------------------------------------------------------------ assignment
+    def _neighbors(self, s):
+        nb = self._nb_cache.get(s)
+        if nb is None:
+            nb = self._nb_cache[s] = tt.neighbors(self.space, s)
+        return nb
+
     def _predicted_cost(self, s) -> float:
         best = math.inf
         if self.space is not None:
-            for t in tt.neighbors(self.space, s):
+            for t in self._neighbors(s):
                 c = self.known.get(t)
                 if c is not None and c < best:
                     best = c
@@ -126,7 +133,7 @@ class ShardedEvaluator:
     def __call__(self, states: Sequence) -> List[float]:
         n = len(states)
         wts = self.weights(states) if self.assign == "lpt" else [1.0] * n
-        vals = torch.zeros(2 * n, dtype=torch.float64, device=self.device)   # costs, then seconds
+        vals = [0.0] * (2 * n)                                                # costs, then seconds
         if self.assign == "dynamic":
             key = f"{self.ns}_round{self.rounds}"
             while True:
@@ -146,13 +153,15 @@ class ShardedEvaluator:
                     vals[j], vals[n + j] = c[j], t[j]
                     self.local_evals += 1
         if self.world > 1:
-            dist.all_reduce(vals, op=dist.ReduceOp.MAX, group=self.group)
+            buf = torch.tensor(vals, dtype=torch.float64, device=self.device)
+            dist.all_reduce(buf, op=dist.ReduceOp.MAX, group=self.group)
+            vals = buf.cpu().tolist()
             if self.assign == "dynamic" and self.rank == 0:
                 try:                                     # every rank has left its claim loop
                     self.store.delete_key(f"{self.ns}_round{self.rounds}")
                 except Exception:  # noqa: BLE001 - older stores: keys are namespaced anyway
                     pass
-        out = vals.cpu().tolist()
+        out = vals
         costs = out[:n]
         if not all(c > 0 for c in costs):
             raise RuntimeError(f"sharded round {self.rounds}: a candidate came back unmeasured ({costs})")

@@ -382,7 +382,7 @@ def test_scoring_opts_reading_z12():
     inc = 385e-6
     m = tt.scoring_opts(sp, o, inc)
     assert m.cut_s == pytest.approx(min(max(20 * inc, 1e-3), max(1e-3, 50 * t_roof)))
-    assert m.race_s == pytest.approx(1.25 * inc)
+    assert m.race_s == pytest.approx(1.1 * inc)
     big = tt.scoring_opts(sp, o, 5.0)                  # an incumbent near s0: the absolute cut rules
     assert big.cut_s == pytest.approx(max(1e-3, 50 * t_roof))
     off = tt.scoring_opts(sp, tt.search_opts(family=1, cut_roofline_x=0.0, race_factor=0.0), math.inf)
