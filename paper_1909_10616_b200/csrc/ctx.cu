@@ -101,13 +101,29 @@ void aggregate_repeats(const double* per, int R, tt_sample* out) {
 
 // ---------------------------------------------------------------- scoring budget (Z12)
 double roofline_seconds(const Space& sp, int device) {
-  int sms = 0, khz = 0;
-  if (device < 0 && cudaGetDevice(&device) != cudaSuccess) device = -1;
-  if (device < 0 || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
-      cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device) != cudaSuccess || sms <= 0 || khz <= 0) {
+  // SM count and clock per device, queried once (cudaDevAttrClockRate costs milliseconds)
+  static std::mutex mu;
+  static std::map<int, std::pair<int, int>> cache;
+  if (device < 0 && cudaGetDevice(&device) != cudaSuccess) {
     cudaGetLastError();
-    sms = 148;
-    khz = 1965000;
+    device = -1;
+  }
+  int sms = 148, khz = 1965000;
+  if (device >= 0) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(device);
+    if (it == cache.end()) {
+      int s = 0, k = 0;
+      if (cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
+          cudaDeviceGetAttribute(&k, cudaDevAttrClockRate, device) != cudaSuccess || s <= 0 || k <= 0) {
+        cudaGetLastError();
+        s = 148;
+        k = 1965000;
+      }
+      it = cache.emplace(device, std::make_pair(s, k)).first;
+    }
+    sms = it->second.first;
+    khz = it->second.second;
   }
   const double fpc = sp.family == TT_FAM_BF16_UMMA ? 8192.0 : (sp.family == TT_FAM_TF32_UMMA ? 4096.0 : 256.0);
   return 2.0 * (double)sp.dim[0] * (double)sp.dim[1] * (double)sp.dim[2] / ((double)sms * khz * 1e3 * fpc);

@@ -412,6 +412,9 @@ __device__ __forceinline__ void mma_role(const UmmaArgs& p, const MmaCtx& c) {
   Sched sch(p, c.cluster_id, c.num_clusters);
   Item it;
   int item_no = 0;
+  if (p.trace && elect_one())                                // debug: MMA role set up (item 5, slot 7)
+    p.trace[((int64_t)c.cluster_id * kTraceItems + 5) * 8 + 7] = globaltimer();
+  __syncwarp();
   while (sch.next(p, &it)) {
     mbar_wait(c.tempty0 + 8u * acc, aphase ^ 1u);
     tc_fence_after();
@@ -503,6 +506,8 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
       mbar_init(tempty0 + 8u * b, kEpiWarps * CG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (p.trace && leader)                                   // debug: barriers initialised (item 2, slot 7)
+      p.trace[((int64_t)(blockIdx.x / CG) * kTraceItems + 2) * 8 + 7] = globaltimer();
   }
   if (warp == 2) {
     if constexpr (CG == 1) {
@@ -512,11 +517,15 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
       asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(p.tmem_cols));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     }
+    if (p.trace && leader && lane == 0)                      // debug: TMEM allocated (item 3, slot 7)
+      p.trace[((int64_t)(blockIdx.x / CG) * kTraceItems + 3) * 8 + 7] = globaltimer();
   }
   tc_fence_before();
   if (csize > 1) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (p.trace && warp == 0 && lane == 0 && leader)          // debug: prologue barrier passed (item 4, slot 7)
+    p.trace[((int64_t)(blockIdx.x / CG) * kTraceItems + 4) * 8 + 7] = globaltimer();
 
   const int cluster_id = blockIdx.x / csize;
   const int num_clusters = gridDim.x / csize;

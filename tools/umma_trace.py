@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--config", required=True)
     ap.add_argument("--out", default="gpurun_out/umma_trace.bin")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--flush", action="store_true", help="256 MiB memset before every launch (bench protocol)")
     a = ap.parse_args()
     if os.path.exists(a.out):
         os.remove(a.out)
@@ -34,7 +35,11 @@ def main():
     A = torch.randn(a.m, a.k, device="cuda").to(dt)
     B = torch.randn(a.k, a.n, device="cuda").to(dt)
     C = torch.empty(a.m, a.n, device="cuda")
-    for _ in range(a.reps):
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if a.flush else None
+    for r in range(a.reps):
+        if flush is not None:
+            flush.fill_(r & 0xFF)
+            torch.cuda.synchronize()
         tt.gemm(A, B, C, fam, s)
     torch.cuda.synchronize()
     raw = np.fromfile(a.out, dtype=np.uint64)
@@ -56,6 +61,12 @@ def main():
         print(f"clusters {ncl} dp_tiles {dp} sk_tiles {sk} kernel span {(end - t0) / 1e3:.2f} us; "
               f"entry {(entry.min() - t0) / 1e3:.2f} .. {(entry.max() - t0) / 1e3:.2f} us, "
               f"teardown passed {(teardown.max() - t0) / 1e3:.2f} us (relative to the first MMA)")
+        for k, what in ((2, "barriers initialised"), (3, "TMEM allocated"), (4, "prologue barrier passed"),
+                        (5, "MMA role set up")):
+            v = tr[:, k, 7]
+            v = v[v > 0]
+            if v.size:
+                print(f"  {what}: {(v.min() - t0) / 1e3:.2f} .. {(v.max() - t0) / 1e3:.2f} us")
         ends = []
         for c in range(ncl):
             items = []
