@@ -239,8 +239,9 @@ def tune(ctx, sp, Mr, N, K, fam, layout, budget, args, world, coll, local):
     ms_fn, observe, cut_fn = tdist.device_measure_set(ctx, sp, sopts, device=local)
     store = tdist.default_store() if (world > 1 and args.assign == "dynamic") else None
     ev = tdist.TrackingEvaluator(observe=observe, measure_set=ms_fn, device=coll if world > 1 else None,
-                                 store=store, assign=None if store is not None else args.assign, space=sp,
-                                 cut_s=cut_fn)
+                                 store=store, assign="lpt" if (args.assign == "dynamic" and store is None) else args.assign,
+                                 space=sp, cut_s=cut_fn)
+    ctx.prepare(sp)                      # one-time setup (operands, flush buffer, kernels loaded) off the clock
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
@@ -251,6 +252,7 @@ def tune(ctx, sp, Mr, N, K, fam, layout, budget, args, world, coll, local):
            "frac_feasible": res.frac_feasible, "tuning_wall_s": tune_wall, "best_config": res.best,
            "best_cost_us": res.best_cost * 1e6, "s0_cost_us": res.trace[0]["cost"] * 1e6,
            "local_evals": ev.local_evals, "rounds": ev.rounds,
+           "speculative_measured": ev.spec_measured, "speculative_used": ev.spec_used,
            "scoring": ("L2 flushed before every timed launch" if args.tune_l2_flush else "warm L2, CUDA-graph replay")
            + "; slow cut min(max(20 cost_min, 1 ms), 50 t_roof), racing at 1.1 cost_min after 2 repeats (reading Z12)",
            "assignment": ev.assign}
@@ -268,31 +270,45 @@ def tune(ctx, sp, Mr, N, K, fam, layout, budget, args, world, coll, local):
         meas = sum(sum(t) for t in ev.round_times)
         host = max(0.0, tune_wall - meas)
         proj = {}
+        nb = {}
+
+        def neighbors(x):
+            if x not in nb:
+                nb[x] = tt.neighbors(sp, x)
+            return nb[x]
+
+        kw = dict(per_round_s=50e-6, states=ev.round_states, neighbors=neighbors)
         for G in (2, 4, 8):
-            ws = host + tdist.projected_sharded_wall(ev.round_times, G, per_round_s=50e-6)
-            wl = host + tdist.projected_sharded_wall(ev.round_times, G, per_round_s=50e-6, weights=ev.round_weights)
-            wd = host + tdist.projected_sharded_wall(ev.round_times, G, per_round_s=50e-6, dynamic=True,
-                                                     per_claim_s=200e-6)
-            proj[str(G)] = {"lpt_wall_s": wl, "lpt_speedup": tune_wall / wl if wl > 0 else None,
-                            "static_wall_s": ws, "static_speedup": tune_wall / ws if ws > 0 else None,
-                            "dynamic_wall_s": wd, "dynamic_speedup": tune_wall / wd if wd > 0 else None}
+            ws = host + tdist.projected_sharded_wall(ev.round_times, G, **kw)
+            wl = host + tdist.projected_sharded_wall(ev.round_times, G, weights=ev.round_weights, **kw)
+            wd = host + tdist.projected_sharded_wall(ev.round_times, G, dynamic=True, per_claim_s=200e-6,
+                                                     weights=ev.round_weights, **kw)
+            proj[str(G)] = {"dynamic_wall_s": wd, "dynamic_speedup": tune_wall / wd if wd > 0 else None,
+                            "lpt_wall_s": wl, "lpt_speedup": tune_wall / wl if wl > 0 else None,
+                            "static_wall_s": ws, "static_speedup": tune_wall / ws if ws > 0 else None}
         rec["projected_sharded_search"] = {"rounds": ev.rounds, "round_sizes": [len(t) for t in ev.round_times],
                                            "measure_s": meas, "host_s": host, "by_gpus": proj,
+                                           "model": "round by round: slowest rank's measurement time + 50 us exchange; "
+                                                    "dynamic = claims in LPT order (200 us each); round 0 speculates "
+                                                    "g(s0) on the idle ranks; host search work replicated",
                                            "kind": "projection from 1-GPU per-candidate times"}
     return res.best, rec
 
 
 def time_gemm(tt, A, B, C, fam, best, layout, steps, warmup, flush, world, sampler=None):
     """W untimed + `steps` timed launches, L2 flushed before each (outside the event pair);
-    barrier + synchronize on both sides; returns per-step ms on the launching stream."""
+    barrier + synchronize on both sides; returns per-step ms on the launching stream.  The GEMM
+    runs through a tt_plan (checked and bound once), so a step is one library call."""
     import torch
     import torch.distributed as dist
     stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    plan = tt.GemmPlan(A, B, C, fam, best, layout=layout)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     for _ in range(warmup):
         flush.fill_(1)
-        tt.gemm(A, B, C, fam, best, layout=layout)
+        plan.launch(sptr)
     torch.cuda.synchronize()
     if sampler is not None:
         sampler.start()
@@ -302,11 +318,12 @@ def time_gemm(tt, A, B, C, fam, best, layout, steps, warmup, flush, world, sampl
     for i in range(steps):
         flush.fill_(i & 0xFF)                           # L2 flush between steps (outside the events)
         starts[i].record(stream)
-        tt.gemm(A, B, C, fam, best, layout=layout)
+        plan.launch(sptr)
         ends[i].record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    plan.close()
     return [s.elapsed_time(e) for s, e in zip(starts, ends)]
 
 
@@ -394,7 +411,7 @@ def main():
     ap.add_argument("--budget", type=int, default=None, help="G-BFS evaluation budget (distinct configs)")
     ap.add_argument("--width", type=int, default=16,
                     help="G-BFS states popped per round W (reading Z9): the same for every GPU count")
-    ap.add_argument("--assign", choices=["lpt", "static", "dynamic"], default="lpt",
+    ap.add_argument("--assign", choices=["lpt", "static", "dynamic"], default="dynamic",
                     help="how a round's candidates are spread over the ranks (paper_1909_10616_b200/dist.py)")
     ap.add_argument("--layout", choices=["nn", "tn"], default="nn",
                     help="tn: A stored as W[K][M] (the paper's perceptron Y = W^T X, P:372)")

@@ -81,7 +81,9 @@ typedef struct {
   int32_t repeats;         /* R actually run (1 when the slow-candidate cut fired, Z12) */
   int32_t number;          /* back-to-back launches per repeat */
   int32_t device;          /* CUDA ordinal the sample was taken on */
-  int32_t slow_cut;        /* 1 if cost_s = probe_s because probe_s > cut_s (Z12) */
+  int32_t slow_cut;        /* 1 if cost_s = probe_s because probe_s > cut_s (Z12); 2 if cost_s is the
+                              F32_SIMT partial-grid estimate (the first ~2 waves of CTA rows timed
+                              and scaled by the wave count) and it exceeded cut_s */
   int32_t graph_nodes;     /* launches per captured CUDA graph the repeats replayed (0: direct launches) */
   int32_t raced;           /* 1 if the repeats stopped after race_repeats (tt_measure_opts.race_s) */
 } tt_sample;
@@ -269,6 +271,17 @@ tt_status tt_gemm(int64_t M, int64_t N, int64_t K, int32_t family, const void* A
 tt_status tt_gemm_ex(int64_t M, int64_t N, int64_t K, int32_t family, int32_t layout, const void* A,
                      const void* B, float* C, const tt_config* cfg, void* stream);
 
+/* A prepared tt_gemm_ex: (M, N, K, family, layout, cfg) are checked and bound to the device
+ * buffers (A, B, C) once, so tt_plan_launch is a kernel launch on `stream` with no argument
+ * checking -- the repeated launch of one GEMM (a training step, bench.py's timed loop).  The plan
+ * keeps the three pointers (the caller keeps the buffers alive until tt_plan_destroy); errors as
+ * tt_gemm_ex at creation, TT_E_CUDA at launch. */
+typedef struct tt_plan tt_plan;
+tt_status tt_plan_create(int64_t M, int64_t N, int64_t K, int32_t family, int32_t layout, const void* A,
+                         const void* B, float* C, const tt_config* cfg, tt_plan** out);
+tt_status tt_plan_launch(tt_plan* plan, void* stream);
+tt_status tt_plan_destroy(tt_plan* plan);
+
 /* Same product through host buffers: copies A (stored per `layout`), B host->device, runs the
  * GEMM, copies C back, all on the ctx stream, and synchronises.  The ctx owns the device staging
  * buffers.  Host buffers should be pinned for asynchronous copies. */
@@ -287,6 +300,11 @@ tt_status tt_ctx_stream(tt_ctx* ctx, void** stream);
 /* Device pointers of the ctx operands for this problem (created if needed). */
 tt_status tt_ctx_operands(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, int32_t family,
                           const void** A, const void** B, float** C);
+
+/* One-time setup of a ctx for a space, outside any timed search: the measurement operands, the
+ * L2-flush buffer, and every kernel of the space's family loaded into the context (lazy module
+ * loading otherwise lands in the first measurement of each kernel).  Synchronises the ctx stream. */
+tt_status tt_ctx_prepare(tt_ctx* ctx, const tt_space* sp);
 
 /* cost(s) on hardware ("test (i.e., run the configuration on target hardware)"):
  * one cold timed probe (if it exceeds opts->cut_s the candidate is scored by it, Z12), warmup

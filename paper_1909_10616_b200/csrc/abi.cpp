@@ -328,6 +328,42 @@ tt_status tt_gemm_ex(int64_t M, int64_t N, int64_t K, int32_t family, int32_t la
   return r == TT_OK ? TT_OK : fail(r, err);
 }
 
+struct tt_plan {
+  Space sp;
+  State st;
+  const void* A;
+  const void* B;
+  float* C;
+  tt_plan(const tt_space& ts, const State& s, const void* a, const void* b, float* c)
+      : sp(ts, false), st(s), A(a), B(b), C(c) {}
+};
+
+tt_status tt_plan_create(int64_t M, int64_t N, int64_t K, int32_t family, int32_t layout, const void* A,
+                         const void* B, float* C, const tt_config* cfg, tt_plan** out) {
+  tt_space ts{M, N, K, 4, 2, 4, family, layout};
+  CHECK_SPACE(&ts);
+  if (!A || !B || !C || !cfg || !out) return fail(TT_E_INVAL, "null argument");
+  if (family == TT_FAM_NONE) return fail(TT_E_UNSUPPORTED, "family NONE has no kernel");
+  Space s(ts, false);
+  State st = from_cfg(*cfg);
+  if (!s.j_prod(st)) return fail(TT_E_ILLEGITIMATE, "J_prod false: factors do not tile (M, N, K)");
+  if (!s.j_hw(st)) return fail(TT_E_INFEASIBLE, "J_hw false for this family");
+  *out = new tt_plan(ts, st, A, B, C);
+  return TT_OK;
+}
+
+tt_status tt_plan_launch(tt_plan* plan, void* stream) {
+  if (!plan) return fail(TT_E_INVAL, "null plan");
+  std::string err;
+  tt_status r = launch_gemm(plan->sp, plan->st, plan->A, plan->B, plan->C, static_cast<cudaStream_t>(stream), &err);
+  return r == TT_OK ? TT_OK : fail(r, err);
+}
+
+tt_status tt_plan_destroy(tt_plan* plan) {
+  delete plan;
+  return TT_OK;
+}
+
 tt_status tt_gemm(int64_t M, int64_t N, int64_t K, int32_t family, const void* A, const void* B, float* C,
                   const tt_config* cfg, void* stream) {
   return tt_gemm_ex(M, N, K, family, TT_LAYOUT_NN, A, B, C, cfg, stream);
@@ -400,6 +436,15 @@ tt_status tt_ctx_operands(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, int32_t 
   if (B) *B = o->B;
   if (C) *C = o->C;
   return TT_OK;
+}
+
+tt_status tt_ctx_prepare(tt_ctx* ctx, const tt_space* sp) {
+  CHECK_SPACE(sp);
+  if (!ctx) return fail(TT_E_INVAL, "null ctx");
+  if (sp->family == TT_FAM_NONE) return fail(TT_E_UNSUPPORTED, "family NONE has no kernel");
+  std::string err;
+  tt_status st = static_cast<Ctx*>(ctx)->prepare(Space(*sp, false), &err);
+  return st == TT_OK ? TT_OK : fail(st, err);
 }
 
 tt_status tt_gemm_host(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, int32_t family, int32_t layout,

@@ -70,6 +70,13 @@ tt_status bind(const Space& sp, const State& s, tt_launch_info* info, std::strin
   return TT_E_UNSUPPORTED;
 }
 
+tt_status prepare_gemm(const Space& sp, const State& s, const void* A, const void* B, float* C, std::string* err) {
+  if (sp.family == TT_FAM_F32_SIMT) return simt_prepare(sp, s, err);
+  if (sp.family == TT_FAM_TF32_UMMA || sp.family == TT_FAM_BF16_UMMA) return umma_prepare(sp, s, A, B, C, err);
+  *err = "family has no kernel";
+  return TT_E_UNSUPPORTED;
+}
+
 tt_status launch_gemm(const Space& sp, const State& s, const void* A, const void* B, float* C, cudaStream_t stream,
                       std::string* err) {
   if (sp.family == TT_FAM_F32_SIMT)
@@ -231,6 +238,19 @@ tt_status Ctx::operands(const Space& sp, Operands** out, std::string* err) {
   return TT_OK;
 }
 
+tt_status Ctx::prepare(const Space& sp, std::string* err) {
+  DeviceGuard g(device);
+  if (!cuda_ok(g.status, err, "cudaSetDevice")) return TT_E_CUDA;
+  Operands* o = nullptr;
+  tt_status st = operands(sp, &o, err);
+  if (st != TT_OK) return st;
+  if (sp.family == TT_FAM_F32_SIMT) st = simt_preload(err);
+  else st = umma_preload(sp.family, err);
+  if (st != TT_OK) return st;
+  if (!flush && (st = flush_l2(err)) != TT_OK) return st;     // allocates the flush buffer
+  return cuda_ok(cudaStreamSynchronize(stream), err, "prepare") ? TT_OK : TT_E_CUDA;
+}
+
 tt_status Ctx::flush_l2(std::string* err) {
   if (!flush) {
     int l2 = 0;
@@ -252,6 +272,9 @@ tt_status Ctx::measure(const Space& sp, const State& s, const tt_measure_opts& m
   tt_status st = operands(sp, &o, err);
   if (st != TT_OK) return st;
   auto launch = [&]() { return launch_gemm(sp, s, o->A, o->B, o->C, stream, err); };
+  // host-side setup (plan, tensor maps, module load) before any timed launch: a first-time cost
+  // must not land between the probe's events (it once scored a 190 us s0 as 4.8 ms)
+  if ((st = prepare_gemm(sp, s, o->A, o->B, o->C, err)) != TT_OK) return st;
   // one timed probe first: a slow candidate (reading Z12) is scored by it and costs one launch
   auto timed_once = [&](double* sec) -> tt_status {
     if (mo.l2_flush && (st = flush_l2(err)) != TT_OK) return st;
@@ -264,9 +287,43 @@ tt_status Ctx::measure(const Space& sp, const State& s, const tt_measure_opts& m
     *sec = pm * 1e-3;
     return TT_OK;
   };
+  *out = tt_sample{};
+  // Partial-grid probe (reading Z12): a K1 launch of many waves (the untiled s0 and its
+  // neighbours: millions of one-thread CTAs, seconds per launch) runs only its first ~2 waves of CTA
+  // rows; when that extrapolates past the cut, the candidate is scored by the estimate (slow_cut = 2)
+  // and never runs in full.  CTAs are independent tiles, so a row prefix of the grid is a valid
+  // partial launch, and the waves of such configs take equal time.
+  if (mo.cut_s > 0 && sp.family == TT_FAM_F32_SIMT) {
+    int64_t ctas = 0, slots = 0;
+    if ((st = simt_probe_shape(sp, s, &ctas, &slots, err)) != TT_OK) return st;
+    const int64_t n0 = s.f[2][0];                       // CTAs per grid row (grid.x)
+    if (ctas >= 8 * slots) {
+      const int64_t rows = std::max<int64_t>(1, (2 * slots + n0 - 1) / n0);
+      const double waves_part = std::ceil((double)(rows * n0) / (double)slots);
+      const double waves_all = std::ceil((double)ctas / (double)slots);
+      if (mo.l2_flush && (st = flush_l2(err)) != TT_OK) return st;
+      cudaEventRecord(ev[0], stream);
+      if ((st = simt_launch(sp, s, static_cast<const float*>(o->A), static_cast<const float*>(o->B), o->C, stream, err,
+                            rows)) != TT_OK)
+        return st;
+      cudaEventRecord(ev[1], stream);
+      if (!cuda_ok(cudaEventSynchronize(ev[1]), err, "partial probe")) return TT_E_CUDA;
+      float pm = 0;
+      cudaEventElapsedTime(&pm, ev[0], ev[1]);
+      const double est = pm * 1e-3 * waves_all / waves_part;
+      if (est > mo.cut_s) {
+        out->cost_s = out->mean_s = out->min_s = est;
+        out->probe_s = pm * 1e-3;
+        out->repeats = 1;
+        out->number = 1;
+        out->slow_cut = 2;
+        out->device = device;
+        return TT_OK;
+      }
+    }
+  }
   double probe = 0;
   if ((st = timed_once(&probe)) != TT_OK) return st;
-  *out = tt_sample{};
   out->probe_s = probe;
   out->device = device;
   if (mo.cut_s > 0 && probe > mo.cut_s) {  // Z12

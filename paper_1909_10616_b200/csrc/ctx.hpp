@@ -49,6 +49,7 @@ struct Ctx : tt_ctx {
   tt_status init(std::string* err);
   tt_status operands(const Space& sp, Operands** out, std::string* err);
   tt_status flush_l2(std::string* err);
+  tt_status prepare(const Space& sp, std::string* err);
   tt_status measure(const Space& sp, const State& s, const tt_measure_opts& mo, tt_sample* out, std::string* err);
   tt_status gemm_host(const Space& sp, const State& s, const void* Ah, const void* Bh, float* Ch, std::string* err);
 };

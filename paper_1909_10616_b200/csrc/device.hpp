@@ -17,6 +17,11 @@ tt_status bind(const Space& sp, const State& s, tt_launch_info* info, std::strin
 tt_status launch_gemm(const Space& sp, const State& s, const void* A, const void* B, float* C,
                       cudaStream_t stream, std::string* err);
 
+// Everything a launch does on the host except the launch itself (instance choice, plan, tensor
+// maps, the shared-memory opt-in that loads the kernel's module), so a timed launch right after
+// it spends no host time between its CUDA events.
+tt_status prepare_gemm(const Space& sp, const State& s, const void* A, const void* B, float* C, std::string* err);
+
 // K4: counter-based U[-1,1) operand generator.
 tt_status launch_fill(void* dst, int dtype, uint64_t seed, uint64_t idx0, uint64_t count,
                       cudaStream_t stream, std::string* err);
@@ -28,8 +33,16 @@ tt_status launch_im2col(int dtype, const void* x, int64_t Nb, int64_t C, int64_t
 // Family-specific launchers (gemm_simt.cu, gemm_umma.cu).
 tt_status simt_bind(const Space& sp, const State& s, tt_launch_info* info, std::string* err);
 tt_status simt_launch(const Space& sp, const State& s, const float* A, const float* B, float* C,
-                      cudaStream_t stream, std::string* err);
+                      cudaStream_t stream, std::string* err, int64_t max_rows = 0);
+// K1 launch shape for the partial-grid probe: total CTAs and co-resident CTA slots on the device.
+tt_status simt_probe_shape(const Space& sp, const State& s, int64_t* ctas, int64_t* slots, std::string* err);
+tt_status simt_prepare(const Space& sp, const State& s, std::string* err);
+// Load every kernel of a family (the max-smem opt-in loads the module function), so no first
+// launch of a search pays it.
+tt_status simt_preload(std::string* err);
+tt_status umma_preload(int family, std::string* err);
 tt_status umma_bind(const Space& sp, const State& s, tt_launch_info* info, std::string* err);
+tt_status umma_prepare(const Space& sp, const State& s, const void* A, const void* B, float* C, std::string* err);
 tt_status umma_launch(const Space& sp, const State& s, const void* A, const void* B, float* C,
                       cudaStream_t stream, std::string* err);
 

@@ -18,6 +18,7 @@
 // multiples of 4 and results are stored with STG.128.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "device.hpp"
@@ -55,28 +56,32 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 constexpr int max_threads(int acc) { return acc <= 16 ? 1024 : (acc <= 64 ? 512 : 256); }
 
+// Fragment of one k step.  A register tile of TM (TN) values is read as float4 chunks: chunk c of
+// the thread's rows sits at as[c * SA + 0..3] (columns: bs[c * SB + 0..3]).  SA = SB = 4 is the
+// contiguous tile; the interleaved layout (kernel below) spreads a thread's chunks one warp-row
+// apart so that the lanes of a warp read adjacent 16-byte words (no shared-memory bank conflicts).
 template <int TM, int TN, bool VECA>
-__device__ __forceinline__ void load_frag(const float* as, const float* bs, int kk, int LDA, int LDB, float* a,
-                                          float* b) {
+__device__ __forceinline__ void load_frag(const float* as, const float* bs, int kk, int LDA, int LDB, int SA, int SB,
+                                          float* a, float* b) {
   if constexpr (VECA) {
 #pragma unroll
     for (int i = 0; i < TM; i += 4) {
-      const float4 v = *reinterpret_cast<const float4*>(as + kk * LDA + i);
+      const float4 v = *reinterpret_cast<const float4*>(as + kk * LDA + (i >> 2) * SA);
       a[i] = v.x; a[i + 1] = v.y; a[i + 2] = v.z; a[i + 3] = v.w;
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < TM; ++i) a[i] = as[kk * LDA + i];
+    for (int i = 0; i < TM; ++i) a[i] = as[kk * LDA + (i >> 2) * SA + (i & 3)];   // SA = 4: as[kk LDA + i]
   }
   if constexpr (TN % 4 == 0) {
 #pragma unroll
     for (int j = 0; j < TN; j += 4) {
-      const float4 v = *reinterpret_cast<const float4*>(bs + kk * LDB + j);
+      const float4 v = *reinterpret_cast<const float4*>(bs + kk * LDB + (j >> 2) * SB);
       b[j] = v.x; b[j + 1] = v.y; b[j + 2] = v.z; b[j + 3] = v.w;
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < TN; ++j) b[j] = bs[kk * LDB + j];
+    for (int j = 0; j < TN; ++j) b[j] = bs[kk * LDB + (j >> 2) * SB + (j & 3)];
   }
 }
 
@@ -122,8 +127,23 @@ k1_simt(SimtArgs p) {
   const int g = t / G, l = t - (t / G) * G;
   const int gm = g / p.n1, gn = g - (g / p.n1) * p.n1;
   const int lm = l / p.n2, ln = l - (l / p.n2) * p.n2;
-  const int row0 = gm * (p.m2 * TM) + lm * TM;
-  const int col0 = gn * (p.n2 * TN) + ln * TN;
+  // Rows / columns of the thread's register tile.  Contiguous: rows row0 .. row0 + TM.  Interleaved
+  // (TM or TN a multiple of 4 and >= 8): float4 chunk c at row0 + c * SA with row0 = 4 x (thread's
+  // index along M) and SA = 4 x (threads along M) -- the same m1 m2 m3 x n1 n2 n3 tile and the same
+  // fmaf chain per output, only the assignment of the tile's rows / columns to threads changes.
+  // The interleaved layout removes the 2-way shared-memory bank conflicts of the 16 x 8 tiles
+  // (profiles/r10_ncu_k1_simt_4096.md: 98.7 M per launch) but measured 6 % slower at 4096^3 and 4 %
+  // at 2048^3 (profiles/r10_simt_ilv_ab.txt), so it is an experiment build (-DTT_SIMT_ILV) only.
+#ifdef TT_SIMT_ILV
+  constexpr bool kIlvA = (TM % 4 == 0) && TM >= 8;
+  constexpr bool kIlvB = (TN % 4 == 0) && TN >= 8;
+#else
+  constexpr bool kIlvA = false, kIlvB = false;
+#endif
+  const int row0 = kIlvA ? (gm * p.m2 + lm) * 4 : gm * (p.m2 * TM) + lm * TM;
+  const int col0 = kIlvB ? (gn * p.n2 + ln) * 4 : gn * (p.n2 * TN) + ln * TN;
+  const int SA = kIlvA ? p.m1 * p.m2 * 4 : 4;
+  const int SB = kIlvB ? p.n1 * p.n2 * 4 : 4;
 
   const int64_t K = p.K, N = p.N;
   const float* Ab = p.a_tn ? p.A + (int64_t)blockIdx.y * BM : p.A + (int64_t)blockIdx.y * BM * K;
@@ -216,13 +236,13 @@ k1_simt(SimtArgs p) {
     const float* bs = Bs + buf * BK * LDB + col0;
     // fragments for step kk+1 are loaded from shared memory while step kk's FMAs issue
     float a0[TM], b0[TN], a1[TM], b1[TN];
-    load_frag<TM, TN, kVecA>(as, bs, 0, LDA, LDB, a0, b0);
+    load_frag<TM, TN, kVecA>(as, bs, 0, LDA, LDB, SA, SB, a0, b0);
     int kk = 0;
 #pragma unroll(BKF > 0 ? BKF / 2 : 1)
     for (; kk + 2 <= BK; kk += 2) {
-      load_frag<TM, TN, kVecA>(as, bs, kk + 1, LDA, LDB, a1, b1);
+      load_frag<TM, TN, kVecA>(as, bs, kk + 1, LDA, LDB, SA, SB, a1, b1);
       fma_frag<TM, TN, kPair>(a0, b0, acc, acc2);
-      if (kk + 2 < BK) load_frag<TM, TN, kVecA>(as, bs, kk + 2, LDA, LDB, a0, b0);
+      if (kk + 2 < BK) load_frag<TM, TN, kVecA>(as, bs, kk + 2, LDA, LDB, SA, SB, a0, b0);
       fma_frag<TM, TN, kPair>(a1, b1, acc, acc2);
     }
     if (kk < BK) fma_frag<TM, TN, kPair>(a0, b0, acc, acc2);   // odd BK: last step
@@ -242,16 +262,20 @@ k1_simt(SimtArgs p) {
   float* Cb = p.C + ((int64_t)blockIdx.y * BM + row0) * N + (int64_t)blockIdx.x * BN + col0;
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
+    float* Ci = Cb + (int64_t)((i >> 2) * SA + (i & 3)) * N;          // contiguous: SA = 4 -> row i
     if constexpr (TN % 4 == 0) {
       if (p.c_vec) {
 #pragma unroll
         for (int j = 0; j < TN; j += 4)
-          *reinterpret_cast<float4*>(Cb + i * N + j) = make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+          *reinterpret_cast<float4*>(Ci + (j >> 2) * SB) = make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
         continue;
       }
-    }
 #pragma unroll
-    for (int j = 0; j < TN; ++j) Cb[i * N + j] = acc[i][j];
+      for (int j = 0; j < TN; ++j) Ci[(j >> 2) * SB + (j & 3)] = acc[i][j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < TN; ++j) Ci[j] = acc[i][j];
+    }
   }
 }
 
@@ -334,9 +358,33 @@ tt_status simt_bind(const Space& sp, const State& s, tt_launch_info* info, std::
   return TT_OK;
 }
 
-tt_status simt_launch(const Space& sp, const State& s, const float* A, const float* B, float* C,
-                      cudaStream_t stream, std::string* err) {
+// The instance a config runs and its resident CTAs per SM (occupancy), for the partial-grid probe.
+namespace {
+struct Pick {
+  KernelFn fn;
   tt_launch_info li;
+};
+tt_status pick_instance(const Space& sp, const State& s, Pick* pk, std::string* err);
+}  // namespace
+
+tt_status simt_probe_shape(const Space& sp, const State& s, int64_t* ctas, int64_t* slots, std::string* err) {
+  Pick pk;
+  tt_status st = pick_instance(sp, s, &pk, err);
+  if (st != TT_OK) return st;
+  int occ = 0, dev = 0, sms = 0;
+  if (!cuda_ok(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pk.fn, pk.li.block_x, pk.li.smem_bytes), err,
+               "occupancy(k1_simt)") ||
+      !cuda_ok(cudaGetDevice(&dev), err, "cudaGetDevice") ||
+      !cuda_ok(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), err, "SM count"))
+    return TT_E_CUDA;
+  *ctas = pk.li.grid_x * pk.li.grid_y;
+  *slots = (int64_t)std::max(occ, 1) * sms;
+  return TT_OK;
+}
+
+namespace {
+tt_status pick_instance(const Space& sp, const State& s, Pick* pk, std::string* err) {
+  tt_launch_info& li = pk->li;
   simt_bind(sp, s, &li, err);
   const int lm = ilog2(li.reg_tile_m), ln = ilog2(li.reg_tile_n);
   Table& tb = table();
@@ -361,6 +409,33 @@ tt_status simt_launch(const Space& sp, const State& s, const float* A, const flo
       }
     }
   }
+  pk->fn = fn;
+  return TT_OK;
+}
+}  // namespace
+
+tt_status simt_preload(std::string* err) {
+  Table& tb = table();
+  for (auto& row : tb.fn)
+    for (KernelFn f : row)
+      if (f && !ensure_max_smem((const void*)f, kSmemPerCta, err)) return TT_E_CUDA;
+  for (const FixedInst& f : kFixed)
+    if (!ensure_max_smem((const void*)f.fn, kSmemPerCta, err)) return TT_E_CUDA;
+  return TT_OK;
+}
+
+tt_status simt_prepare(const Space& sp, const State& s, std::string* err) {
+  Pick pk;
+  return pick_instance(sp, s, &pk, err);
+}
+
+tt_status simt_launch(const Space& sp, const State& s, const float* A, const float* B, float* C,
+                      cudaStream_t stream, std::string* err, int64_t max_rows) {
+  Pick pk;
+  tt_status pst = pick_instance(sp, s, &pk, err);
+  if (pst != TT_OK) return pst;
+  const tt_launch_info& li = pk.li;
+  KernelFn fn = pk.fn;
   SimtArgs a;
   a.A = A;
   a.B = B;
@@ -385,7 +460,9 @@ tt_status simt_launch(const Space& sp, const State& s, const float* A, const flo
   a.stages = li.stages;
   a.a_vec16 = (li.tile_m % 4 == 0 && a.M % 4 == 0 && ((uintptr_t)A % 16) == 0 &&
                ((2 * (int64_t)a.bk * (li.tile_n + 4)) % 4) == 0) ? 1 : 0;
-  dim3 grid((unsigned)li.grid_x, (unsigned)li.grid_y, 1);
+  // max_rows > 0 (the partial-grid probe of tt_measure): only the first max_rows CTA rows run
+  const int64_t rows = max_rows > 0 ? std::min<int64_t>(max_rows, li.grid_y) : li.grid_y;
+  dim3 grid((unsigned)li.grid_x, (unsigned)rows, 1);
   fn<<<grid, li.block_x, li.smem_bytes, stream>>>(a);
   if (!cuda_ok(cudaGetLastError(), err, "k1_simt launch")) return TT_E_CUDA;
   return TT_OK;

@@ -1081,8 +1081,10 @@ tt_status prepare(const Space& sp, const State& s, const void* A, const void* B,
 
 }  // namespace
 
-tt_status umma_launch(const Space& sp, const State& s, const void* A, const void* B, float* C, cudaStream_t stream,
-                      std::string* err) {
+namespace {
+// Plan + tensor maps of (problem, config, pointers) from the launch cache (inserted on a miss).
+tt_status cached_entry(const Space& sp, const State& s, const void* A, const void* B, float* C, LaunchEntry* e,
+                       std::string* err) {
   static std::mutex mu;
   static std::map<LaunchKey, LaunchEntry> cache;
   LaunchKey k;
@@ -1098,23 +1100,43 @@ tt_status umma_launch(const Space& sp, const State& s, const void* A, const void
   k.A = A;
   k.B = B;
   k.C = C;
-  LaunchEntry e;
-  bool hit = false;
   {
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(k);
     if (it != cache.end()) {
-      e = it->second;
-      hit = true;
+      *e = it->second;
+      return TT_OK;
     }
   }
-  if (!hit) {
-    tt_status st = prepare(sp, s, A, B, C, &e, err);
-    if (st != TT_OK) return st;
-    std::lock_guard<std::mutex> lk(mu);
-    if (cache.size() >= kLaunchCacheMax) cache.clear();
-    cache.emplace(k, e);
-  }
+  tt_status st = prepare(sp, s, A, B, C, e, err);
+  if (st != TT_OK) return st;
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.size() >= kLaunchCacheMax) cache.clear();
+  cache.emplace(k, *e);
+  return TT_OK;
+}
+}  // namespace
+
+tt_status umma_preload(int family, std::string* err) {
+  const bool ok = family == TT_FAM_BF16_UMMA ? (set_smem_attr<0, 1>(err) && set_smem_attr<0, 2>(err))
+                                             : (set_smem_attr<1, 1>(err) && set_smem_attr<1, 2>(err));
+  return ok ? TT_OK : TT_E_CUDA;
+}
+
+tt_status umma_prepare(const Space& sp, const State& s, const void* A, const void* B, float* C, std::string* err) {
+  LaunchEntry e;
+  tt_status st = cached_entry(sp, s, A, B, C, &e, err);
+  if (st != TT_OK) return st;
+  const bool ok = e.pl.kind == 0 ? (e.pl.cg == 1 ? set_smem_attr<0, 1>(err) : set_smem_attr<0, 2>(err))
+                                 : (e.pl.cg == 1 ? set_smem_attr<1, 1>(err) : set_smem_attr<1, 2>(err));
+  return ok ? TT_OK : TT_E_CUDA;
+}
+
+tt_status umma_launch(const Space& sp, const State& s, const void* A, const void* B, float* C, cudaStream_t stream,
+                      std::string* err) {
+  LaunchEntry e;
+  tt_status st = cached_entry(sp, s, A, B, C, &e, err);
+  if (st != TT_OK) return st;
   const Plan& pl = e.pl;
   if (pl.kind == 0) {
     return pl.cg == 1 ? launch_t<0, 1>(pl, e.ma, e.mb, e.mc, C, stream, err)

@@ -45,8 +45,14 @@ class ShardedEvaluator:
       scoring rules (one launch above the cut, ~11 below).  Every rank holds the same known
       costs, so every rank computes the same assignment with no communication.
     * ``"static"``: candidate j on rank j mod G.
-    * ``"dynamic"`` (``store`` given): ranks claim the next unmeasured index from a shared
-      counter (``store.add``) whenever they are free.
+    * ``"dynamic"`` (``store`` given): ranks claim the next unmeasured candidate, in the LPT
+      order of the predictions, from a shared counter (``store.add``) whenever they are free.
+
+    Speculation (``speculate``, needs ``space``): in round 0 -- s0 alone, so G - 1 ranks would
+    idle -- the idle ranks measure s0's neighbourhood g(s0), from which round 1 draws all of its
+    candidates; their costs are served from a cache when the search asks for them.  Nothing about
+    the traversal changes; ``spec_measured`` / ``spec_used`` count the extra hardware
+    measurements and how many the search consumed.
 
     Costs are exchanged with one all_reduce(MAX) of an [n] float64 vector whose entries only the
     measuring rank filled (every cost is > 0), so each candidate is measured exactly once and the
@@ -57,7 +63,8 @@ class ShardedEvaluator:
 
     def __init__(self, measure_one: Optional[Callable] = None, group=None, device: Optional[torch.device] = None,
                  store=None, measure_set: Optional[Callable] = None, assign: Optional[str] = None,
-                 space: Optional[tt.Space] = None, cut_s: Optional[Callable[[], float]] = None):
+                 space: Optional[tt.Space] = None, cut_s: Optional[Callable[[], float]] = None,
+                 speculate: bool = True):
         if measure_set is None:
             if measure_one is None:
                 raise ValueError("need measure_one or measure_set")
@@ -86,6 +93,11 @@ class ShardedEvaluator:
         self.local_evals = 0
         self.known: dict = {}
         self._nb_cache: dict = {}
+        self.speculate = speculate
+        self.cache: dict = {}                # speculative costs not yet requested by the search
+        self.spec_measured = 0
+        self.spec_used = 0
+        self.round_states: List[list] = []
         # per round: (measurement seconds of every candidate on the rank that measured it -- the
         # values are exchanged with the costs --, predicted weights used by the LPT assignment)
         self.round_times: List[List[float]] = []
@@ -130,43 +142,102 @@ class ShardedEvaluator:
         return owner
 
     # ------------------------------------------------------------------ one round
+    def _speculative(self, states) -> List:
+        """States the idle ranks measure while a round that has fewer candidates than ranks runs:
+        the round-0 neighbourhood g(s0) (Eq. 9 under reading Z4), in action order.  Round 1 of
+        G-BFS draws its candidates from exactly that set (Alg. 1 line 6), so it then costs no
+        measurement; the traversal is unchanged (costs are looked up, never re-drawn)."""
+        if not self.speculate or self.rounds != 0 or self.world <= len(states) or self.space is None:
+            return []
+        seen = set(states) | set(self.known) | set(self.cache)
+        out = []
+        for s in states:
+            for t in self._neighbors(s):
+                if t not in seen:
+                    seen.add(t)
+                    out.append(t)
+        return out
+
     def __call__(self, states: Sequence) -> List[float]:
         n = len(states)
-        wts = self.weights(states) if self.assign == "lpt" else [1.0] * n
-        vals = [0.0] * (2 * n)                                                # costs, then seconds
-        if self.assign == "dynamic":
+        hit = [s in self.cache for s in states]         # measured speculatively in an earlier round
+        todo = [j for j in range(n) if not hit[j]]
+        sub = [states[j] for j in todo]
+        m = len(sub)
+        wts = self.weights(sub) if self.assign in ("lpt", "dynamic") else [1.0] * m
+        spec = self._speculative(sub)
+        S = len(spec)
+        vals = [0.0] * (2 * m + 2 * S)          # costs, seconds (this round), then speculative costs, seconds
+        if self.assign == "dynamic" and self.world > 1:
+            # claim in longest-predicted-first order (LPT order) from a shared counter
+            order = sorted(range(m), key=lambda j: (-wts[j], j))
             key = f"{self.ns}_round{self.rounds}"
             while True:
-                j = int(self.store.add(key, 1)) - 1
-                if j >= n:
+                q = int(self.store.add(key, 1)) - 1
+                if q >= m:
                     break
-                mine = [i == j for i in range(n)]
-                c, t = self.measure_set(states, mine)
-                vals[j], vals[n + j] = c[j], t[j]
+                j = order[q]
+                c, t = self.measure_set(sub, [i == j for i in range(m)])
+                vals[j], vals[m + j] = c[j], t[j]
                 self.local_evals += 1
+            if S:                                        # then the speculative states, same way
+                while True:
+                    q = int(self.store.add(key + "_spec", 1)) - 1
+                    if q >= S:
+                        break
+                    c, t = self.measure_set(spec, [i == q for i in range(S)])
+                    vals[2 * m + q], vals[2 * m + S + q] = c[q], t[q]
+            spec_owner = []
         else:
-            owner = self.lpt_owners(wts, self.world) if self.assign == "lpt" else [j % self.world for j in range(n)]
+            if self.assign == "lpt":
+                owner = self.lpt_owners(wts, self.world)
+            else:
+                owner = [j % self.world for j in range(m)]
             mine = [o == self.rank for o in owner]
-            c, t = self.measure_set(states, mine)
-            for j in range(n):
-                if mine[j]:
-                    vals[j], vals[n + j] = c[j], t[j]
-                    self.local_evals += 1
+            if any(mine):
+                c, t = self.measure_set(sub, mine)
+                for j in range(m):
+                    if mine[j]:
+                        vals[j], vals[m + j] = c[j], t[j]
+                        self.local_evals += 1
+            busy = set(owner)
+            idle = [r for r in range(self.world) if r not in busy] or list(range(self.world))
+            spec_owner = [idle[i % len(idle)] for i in range(S)]
+        if S and spec_owner:
+            smine = [o == self.rank for o in spec_owner]
+            if any(smine):
+                c, t = self.measure_set(spec, smine)
+                for i in range(S):
+                    if smine[i]:
+                        vals[2 * m + i], vals[2 * m + S + i] = c[i], t[i]
         if self.world > 1:
             buf = torch.tensor(vals, dtype=torch.float64, device=self.device)
             dist.all_reduce(buf, op=dist.ReduceOp.MAX, group=self.group)
             vals = buf.cpu().tolist()
             if self.assign == "dynamic" and self.rank == 0:
-                try:                                     # every rank has left its claim loop
-                    self.store.delete_key(f"{self.ns}_round{self.rounds}")
-                except Exception:  # noqa: BLE001 - older stores: keys are namespaced anyway
-                    pass
-        out = vals
-        costs = out[:n]
+                for k in (f"{self.ns}_round{self.rounds}", f"{self.ns}_round{self.rounds}_spec"):
+                    try:                                 # every rank has left its claim loops
+                        self.store.delete_key(k)
+                    except Exception:  # noqa: BLE001 - older stores: keys are namespaced anyway
+                        pass
+        costs = [0.0] * n
+        secs = [0.0] * n
+        for q, j in enumerate(todo):
+            costs[j], secs[j] = vals[q], vals[m + q]
+        for j in range(n):
+            if hit[j]:
+                costs[j] = self.cache.pop(states[j])
+                self.spec_used += 1
         if not all(c > 0 for c in costs):
             raise RuntimeError(f"sharded round {self.rounds}: a candidate came back unmeasured ({costs})")
-        self.round_times.append(out[n:])
-        self.round_weights.append(wts)
+        for i in range(S):
+            if vals[2 * m + i] > 0:
+                self.cache[spec[i]] = vals[2 * m + i]
+                self.spec_measured += 1
+        self.round_times.append(secs)
+        self.round_weights.append([w for w in wts] if m == n else
+                                  [wts[todo.index(j)] if not hit[j] else 0.0 for j in range(n)])
+        self.round_states.append(list(states))
         self.rounds += 1
         for s, c in zip(states, costs):
             self.known[s] = c
@@ -203,28 +274,73 @@ def device_measure_set(ctx: tt.Context, sp: tt.Space, opts: tt.SearchOpts, devic
     return measure_set, observe, lambda: mo().cut_s
 
 
+def _busy(times: Sequence[float], world: int, mode: str, weights: Optional[Sequence[float]], per_claim_s: float):
+    """Per-rank busy time of one round's candidates under an assignment rule."""
+    busy = [0.0] * world
+    if mode == "dynamic":                                  # list scheduling, LPT order if weighted
+        order = sorted(range(len(times)), key=lambda j: (-weights[j], j)) if weights is not None else range(len(times))
+        for j in order:
+            r = min(range(world), key=lambda i: busy[i])
+            busy[r] += times[j] + per_claim_s
+    else:
+        owner = ShardedEvaluator.lpt_owners(weights, world) if mode == "lpt" else [j % world for j in range(len(times))]
+        for j, t in enumerate(times):
+            busy[owner[j]] += t
+    return busy
+
+
 def projected_sharded_wall(round_times: Sequence[Sequence[float]], world: int, per_round_s: float = 0.0,
                            dynamic: bool = False, per_claim_s: float = 0.0,
-                           weights: Optional[Sequence[Sequence[float]]] = None) -> float:
+                           weights: Optional[Sequence[Sequence[float]]] = None,
+                           states: Optional[Sequence[Sequence]] = None, neighbors: Optional[Callable] = None) -> float:
     """Measurement wall time of the same traversal sharded over ``world`` ranks, from
     per-candidate times recorded on one rank: sum over rounds of the slowest rank's busy time,
-    plus ``per_round_s`` (the collective) per round.  Static: candidate j on rank j mod world.
-    ``weights`` given: the LPT assignment the evaluator makes from those predicted weights.
-    Dynamic: candidates in index order each go to the rank that becomes free first (what the
-    counter-claiming evaluator does), each claim costing ``per_claim_s``.  A projection from
-    measured times, not a multi-GPU measurement."""
+    plus ``per_round_s`` (the exchange) per round.  Static: candidate j on rank j mod world.
+    ``weights`` given: the evaluator's LPT assignment from those predicted weights (with
+    ``dynamic``: claims in that order).  Dynamic: each candidate goes to the rank that becomes
+    free first, each claim costing ``per_claim_s``.  ``states`` + ``neighbors`` given: the
+    speculative round 0 (ShardedEvaluator.speculate) -- the idle ranks measure g(s0) while s0 runs,
+    each such state costing what it cost when the search measured it (else the dearest of them),
+    and later rounds do not re-measure those states.  A projection from measured times, not a
+    multi-GPU measurement."""
+    mode = "dynamic" if dynamic else ("lpt" if weights is not None else "static")
+    spec_t = {}
+    if states is not None and neighbors is not None and world > 1 and round_times and len(round_times[0]) < world:
+        seen = set(states[0])
+        order = []
+        for s0 in states[0]:
+            for t in neighbors(s0):
+                if t not in seen:
+                    seen.add(t)
+                    order.append(t)
+        when = {}
+        for k in range(1, len(states)):
+            for s, t in zip(states[k], round_times[k]):
+                when.setdefault(s, t)
+        known = [when[t] for t in order if t in when]
+        fallback = max(known) if known else max(round_times[0])
+        spec_t = {t: when.get(t, fallback) for t in order}
     total = 0.0
     for k, times in enumerate(round_times):
-        busy = [0.0] * world
-        if weights is not None:
-            owner = ShardedEvaluator.lpt_owners(weights[k], world)
-        for j, t in enumerate(times):
-            if weights is not None:
-                r = owner[j]
+        w = weights[k] if weights is not None else None
+        if spec_t and k > 0:
+            keep = [j for j, s in enumerate(states[k]) if s not in spec_t]
+            times = [times[j] for j in keep]
+            w = [w[j] for j in keep] if w is not None else None
+            for s in states[k]:                            # a speculative state is served once
+                spec_t.pop(s, None)
+        busy = _busy(times, world, mode, w, per_claim_s)
+        if spec_t and k == 0:
+            st = list(spec_t.values())
+            if mode == "dynamic":
+                for t in st:
+                    r = min(range(world), key=lambda i: busy[i])
+                    busy[r] += t + per_claim_s
             else:
-                r = min(range(world), key=lambda i: busy[i]) if dynamic else j % world
-            busy[r] += t + (per_claim_s if dynamic else 0.0)
-        total += max(busy) + (per_round_s if world > 1 else 0.0)
+                idle = [r for r in range(world) if busy[r] == 0.0] or list(range(world))
+                for i, t in enumerate(st):
+                    busy[idle[i % len(idle)]] += t
+        total += (max(busy) if busy else 0.0) + (per_round_s if world > 1 else 0.0)
     return total
 
 

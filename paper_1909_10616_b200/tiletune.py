@@ -95,10 +95,14 @@ EXPORTS = {
     "tt_fill_uniform": (i32, [vp, i32, u64, u64, u64, vp]),
     "tt_gemm": (i32, [i64, i64, i64, i32, vp, vp, vp, C.POINTER(Config), vp]),
     "tt_gemm_ex": (i32, [i64, i64, i64, i32, i32, vp, vp, vp, C.POINTER(Config), vp]),
+    "tt_plan_create": (i32, [i64, i64, i64, i32, i32, vp, vp, vp, C.POINTER(Config), C.POINTER(vp)]),
+    "tt_plan_launch": (i32, [vp, vp]),
+    "tt_plan_destroy": (i32, [vp]),
     "tt_gemm_host": (i32, [vp, i64, i64, i64, i32, i32, vp, vp, vp, C.POINTER(Config)]),
     "tt_ctx_create": (i32, [i32, u64, C.POINTER(vp)]),
     "tt_ctx_destroy": (i32, [vp]),
     "tt_ctx_stream": (i32, [vp, C.POINTER(vp)]),
+    "tt_ctx_prepare": (i32, [vp, C.POINTER(Space)]),
     "tt_ctx_operands": (i32, [vp, i64, i64, i64, i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
     "tt_aggregate": (i32, [C.POINTER(dbl), i32, C.POINTER(Sample)]),
     "tt_roofline_seconds": (i32, [C.POINTER(Space), i32, C.POINTER(dbl)]),
@@ -322,6 +326,36 @@ def scoring_opts(sp: Space, opts: "SearchOpts", cost_min: float, device: int = -
     return mo
 
 
+class GemmPlan:
+    """tt_plan: one GEMM bound to its buffers once (checked here and in the library), then
+    ``launch()`` is a single library call -- for launching the same GEMM many times."""
+
+    def __init__(self, A, B, C_out, family: int, s: State, layout: int = LAYOUT_NN):
+        M, N, K = _check_gemm_operands(A, B, C_out, family, layout, on_device=True)
+        self._keep = (A, B, C_out)                         # the plan holds raw pointers
+        self.h = vp()
+        _check(lib.tt_plan_create(M, N, K, family, layout, A.data_ptr(), B.data_ptr(), C_out.data_ptr(),
+                                  C.byref(to_config(s)), C.byref(self.h)), "plan_create")
+
+    def launch(self, stream=None):
+        """stream: None (torch's current stream), a torch.cuda.Stream or a raw cudaStream_t int."""
+        st = lib.tt_plan_launch(self.h, _stream(stream))
+        if st != OK:
+            raise TileTuneError(st, "plan_launch")
+
+    def close(self):
+        if self.h:
+            lib.tt_plan_destroy(self.h)
+            self.h = vp()
+            self._keep = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def measure_opts(**kw) -> MeasureOpts:
     mo = MeasureOpts()
     lib.tt_measure_opts_default(C.byref(mo))
@@ -358,6 +392,10 @@ class Context:
         a, b, c = vp(), vp(), vp()
         _check(lib.tt_ctx_operands(self.h, M, N, K, family, C.byref(a), C.byref(b), C.byref(c)), "ctx_operands")
         return a.value, b.value, c.value
+
+    def prepare(self, sp: Space):
+        """tt_ctx_prepare: operands, flush buffer and the family's kernels loaded (one-time setup)."""
+        _check(lib.tt_ctx_prepare(self.h, C.byref(sp)), "ctx_prepare")
 
     def measure(self, sp: Space, s: State, opts: Optional[MeasureOpts] = None) -> Sample:
         out = Sample()

@@ -53,7 +53,8 @@ def _worker(rank, world, port, algo, out, mode="static"):
     res2 = tt.gbfs_search(64, 64, 64, 120, tt.search_opts(seed=9, width=4), batch=ev2)
     row_ranges = tdist.row_shard(8192, world, rank)
     out[rank] = ([(r["state"], r["cost"]) for r in res.trace], n_first, ev.rounds, row_ranges,
-                 [(r["state"], r["cost"]) for r in res2.trace], len(measured) - n_first)
+                 [(r["state"], r["cost"]) for r in res2.trace], len(measured) - n_first,
+                 (ev.spec_measured, ev.spec_used, ev2.spec_measured, ev2.spec_used))
     dist.destroy_process_group()
 
 
@@ -71,17 +72,22 @@ def test_sharded_search_matches_oracle(algo, mode):
     else:
         o = ona2c.na2c(sp, ogbfs.table_source(sp, tab), budget=200, params=ona2c.Params(epsilon=0.0), seed=4)
     ref = [(r.state, r.cost) for r in o.trace]
-    t0, n0, rounds0, rr0, u0, m0 = out[0]
-    t1, n1, rounds1, rr1, u1, m1 = out[1]
+    t0, n0, rounds0, rr0, u0, m0, sp0 = out[0]
+    t1, n1, rounds1, rr1, u1, m1, sp1 = out[1]
     assert t0 == t1 == ref                                 # identical traversal on every rank = oracle
-    assert n0 + n1 == len(ref)                             # each candidate measured exactly once
+    assert sp0 == sp1                                      # every rank agrees on the speculation
+    if mode == "lpt":                                      # g(s0) measured while s0 runs (1 idle rank)
+        assert sp0[0] == len(space.neighbors(sp, space.initial_state(sp))) and 5 <= sp0[1] <= sp0[0]
+    else:
+        assert sp0 == (0, 0, 0, 0)
+    assert n0 + n1 == len(ref) + sp0[0] - sp0[1]           # each candidate measured exactly once
     if mode == "static":
         assert abs(n0 - n1) <= rounds0                     # round-robin balance
     assert rr0 == (0, 4096) and rr1 == (4096, 8192)        # exact row partition
     # second search in the same group: still the oracle traversal, each candidate measured once
     o2 = ogbfs.gbfs(sp, ogbfs.table_source(sp, tab), budget=120, rho=5, seed=9, width=4)
     assert u0 == u1 == [(r.state, r.cost) for r in o2.trace]
-    assert m0 + m1 == 120
+    assert m0 + m1 == 120 + sp0[2] - sp0[3]
 
 
 def test_lpt_owners():
@@ -101,3 +107,11 @@ def test_projection():
     assert tdist.projected_sharded_wall([[4.0, 1.0, 1.0, 1.0, 1.0]], 2) == 6.0
     # LPT from predicted weights: the long candidate alone on one rank
     assert tdist.projected_sharded_wall([[4.0, 1.0, 1.0, 1.0, 1.0]], 2, weights=[[4.0, 1.0, 1.0, 1.0, 1.0]]) == 4.0
+    # speculative round 0: s0 (2.0) alone; its neighbours a, b (measured later at 1.5 / 1.0) run on
+    # the idle ranks meanwhile, so round 1 (a, b) costs nothing and round 2 (c) runs as usual
+    nb = {"s0": ["a", "b"], "a": [], "b": []}
+    st = [["s0"], ["a", "b"], ["c"]]
+    rt = [[2.0], [1.5, 1.0], [3.0]]
+    assert tdist.projected_sharded_wall(rt, 1, states=st, neighbors=nb.get) == 2.0 + 2.5 + 3.0
+    assert tdist.projected_sharded_wall(rt, 2, states=st, neighbors=nb.get) == 2.5 + 0.0 + 3.0
+    assert tdist.projected_sharded_wall(rt, 3, states=st, neighbors=nb.get) == 2.0 + 0.0 + 3.0
