@@ -426,6 +426,9 @@ __device__ __forceinline__ void mma_role(const UmmaArgs& p, const MmaCtx& c) {
     for (int kb = it.kb0; kb < it.kb1; ++kb) {
       mbar_wait(c.full0 + 8u * stage, phase);
       tc_fence_after();
+      if (p.trace && item_no == 1 && kb == it.kb0 && elect_one())   // debug: first stage landed (item 7, slot 7)
+        p.trace[((int64_t)c.cluster_id * kTraceItems + 7) * 8 + 7] = globaltimer();
+      __syncwarp();
       // descriptor start field = CTA-window byte address >> 4 (14 bits): the cvta result of a CTA
       // with cluster rank > 0 carries the rank above bit 24, which must not leak into LBO
       const uint32_t sa16 = ((c.sbase + (uint32_t)stage * p.stage_bytes) >> 4) & 0x3FFFu;
@@ -541,6 +544,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     const int a_kstep = p.swz_a / ELEM;
     Sched sch(p, cluster_id, num_clusters);
     Item it;
+    bool tp_first = true;
     while (sch.next(p, &it)) {
       const int tm = it.tile % p.m0, tn = it.tile / p.m0;
       const int row = tm * (CG * rows_cta) + (int)rank * rows_cta;
@@ -550,6 +554,10 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
         mbar_wait(empty0 + 8u * stage, phase ^ 1u);
         const uint32_t fb = full0 + 8u * stage;
         if (elect_one()) {
+          if (p.trace && leader && tp_first) {             // debug: first TMA issued (item 6, slot 7)
+            p.trace[((int64_t)cluster_id * kTraceItems + 6) * 8 + 7] = globaltimer();
+            tp_first = false;
+          }
           if (leader) mbar_arrive_expect_tx(fb, p.tx_bytes * CG);
           const uint32_t sa = sbase + (uint32_t)stage * p.stage_bytes;
           const uint32_t sb = sa + p.a_stage_bytes;

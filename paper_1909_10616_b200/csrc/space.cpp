@@ -212,6 +212,10 @@ void Space::neighbors(const State& s, std::vector<State>* out) const {
 
 uint64_t Space::count_feasible() const {
   if (family == TT_FAM_NONE) return raw();
+  // Spaces are immutable and cached (Space::get), so the count is computed once: a search's
+  // result (frac_feasible) would otherwise re-enumerate ~2.7M states inside its wall time.
+  const uint64_t memo = feasible_memo_.load(std::memory_order_relaxed);
+  if (memo != ~0ull) return memo;
   uint64_t c = 0;
   State s;
   for (const Vec& vm : lists[0])
@@ -222,6 +226,7 @@ uint64_t Space::count_feasible() const {
         s.f[2] = vn;
         c += j_hw(s);
       }
+  feasible_memo_.store(c, std::memory_order_relaxed);
   return c;
 }
 

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <array>
+#include <atomic>
 #include <cstdint>
 #include <memory>
 #include <string>
@@ -43,11 +44,14 @@ class Space {
   bool legit(const State& s) const { return j_prod(s) && j_hw(s); }
   bool step(const State& s, const Action& a, State* out) const;   // false if s_x[j] odd
   void neighbors(const State& s, std::vector<State>* out) const;  // legit only, action order
-  uint64_t count_feasible() const;
+  uint64_t count_feasible() const;   // enumerates the raw space once, then memoized
   void features(const State& s, double* x) const;                 // log2(f)/log2(dim)
   int nfeat() const { return d[0] + d[1] + d[2]; }
 
   Space(const tt_space& sp, bool build_lists);
+
+ private:
+  mutable std::atomic<uint64_t> feasible_memo_{~0ull};
 };
 
 State from_cfg(const tt_config& c);

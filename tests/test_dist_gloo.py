@@ -115,3 +115,22 @@ def test_projection():
     assert tdist.projected_sharded_wall(rt, 1, states=st, neighbors=nb.get) == 2.0 + 2.5 + 3.0
     assert tdist.projected_sharded_wall(rt, 2, states=st, neighbors=nb.get) == 2.5 + 0.0 + 3.0
     assert tdist.projected_sharded_wall(rt, 3, states=st, neighbors=nb.get) == 2.0 + 0.0 + 3.0
+
+
+def test_predicted_cost_equals_min_over_legit_neighbors():
+    # the LPT prediction walks raw moves (no ctypes); with only legitimate states measured it must
+    # equal the min over g(s) from the library's neighbour function
+    import random
+
+    from paper_1909_10616_b200 import tiletune as tt
+    for fam, M in ((tt.FAM_BF16_UMMA, 4096), (tt.FAM_F32_SIMT, 512)):
+        sp = tt.make_space(M, M, M, family=fam)
+        feas = tt.enumerate_feasible(sp)[0]
+        rng = random.Random(fam)
+        ev = tdist.ShardedEvaluator(lambda s: 1.0, space=sp)
+        ev.known = {s: rng.random() for s in rng.sample(feas, min(len(feas), 150))}
+        for s in rng.sample(feas, 60):
+            nb = [ev.known[t] for t in tt.neighbors(sp, s) if t in ev.known]
+            want = min(nb) if nb else min(ev.known.values())
+            assert ev._predicted_cost(s) == want
+            assert set(tt.neighbors(sp, s)) <= set(ev._moves(s))

@@ -62,7 +62,8 @@ def main():
               f"entry {(entry.min() - t0) / 1e3:.2f} .. {(entry.max() - t0) / 1e3:.2f} us, "
               f"teardown passed {(teardown.max() - t0) / 1e3:.2f} us (relative to the first MMA)")
         for k, what in ((2, "barriers initialised"), (3, "TMEM allocated"), (4, "prologue barrier passed"),
-                        (5, "MMA role set up")):
+                        (5, "MMA role set up"), (6, "first TMA issued"),
+                        (7, "first stage landed")):
             v = tr[:, k, 7]
             v = v[v > 0]
             if v.size:
