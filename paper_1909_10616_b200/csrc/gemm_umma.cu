@@ -71,6 +71,15 @@ struct UmmaArgs {
   uint64_t* trace;                  // debug (TT_UMMA_TRACE): per cluster x item timestamps, or null
 };
 
+// Debug instrumentation is compiled only into the trace build (python -m paper_1909_10616_b200.build
+// --variant trace TT_UMMA_TRACE_BUILD; tools/umma_trace.py loads it): in the product kernel every
+// `kTrace && ...` branch folds away, so the timing code costs neither instructions nor registers.
+#ifdef TT_UMMA_TRACE_BUILD
+constexpr bool kTrace = true;
+#else
+constexpr bool kTrace = false;
+#endif
+
 // TT_UMMA_TRACE layout: [cluster][kTraceItems][8] u64 = tile, kb0 | kb1 << 16 | order << 32,
 // t(MMA start), t(MMA last issue), t(epilogue: accumulator ready), t(epilogue: flag ok), t(done),
 // and in slot 7: kernel entry (item 0) / teardown barrier passed (item 1)
@@ -86,6 +95,11 @@ constexpr int kFlagWords = 1024;    // >= max split tiles (< 148 clusters) x CTA
 __device__ uint32_t g_split_flags[kFlagGroups * kFlagWords];
 
 // ---------------------------------------------------------------- PTX helpers
+// debug (TT_UMMA_TRACE): cycles since kernel entry on this SM, into slot 7 of item 8 + idx
+__device__ __forceinline__ void trace_cycles(uint64_t* trace, int cluster, int idx, long long t_entry) {
+  trace[((int64_t)cluster * 16 + 8 + idx) * 8 + 7] = (uint64_t)(clock64() - t_entry);
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -317,25 +331,28 @@ struct Item {
 };
 
 struct Sched {
+  // 32-bit throughout: the host enables a split only when sk_workers x sk_tiles x k0 < 2^32
+  // (plan_of), and 64-bit divisions (a called subroutine each) cost ~1 us of prologue.
   int w, P, dp, nseg, seg;
-  int64_t b, e;
-  __device__ __forceinline__ static int64_t sk_begin(const UmmaArgs& p, int v) {
-    return (int64_t)v * ((int64_t)p.sk_tiles * p.k0) / p.sk_workers;
+  uint32_t b, e;
+  __device__ __forceinline__ static uint32_t sk_begin(const UmmaArgs& p, int v) {
+    return (uint32_t)v * ((uint32_t)p.sk_tiles * (uint32_t)p.k0) / (uint32_t)p.sk_workers;
   }
   __device__ __forceinline__ Sched(const UmmaArgs& p, int w_, int P_) : w(w_), P(P_), dp(w_), nseg(0), seg(0), b(0), e(0) {
     if (w < p.sk_workers) {
       b = sk_begin(p, w);
       e = sk_begin(p, w + 1);
-      if (e > b) nseg = (int)((e - 1) / p.k0 - b / p.k0) + 1;
+      if (e > b) nseg = (int)((e - 1) / (uint32_t)p.k0 - b / (uint32_t)p.k0) + 1;
     }
   }
   // tail pieces first, last tile of the range first; then the data-parallel tiles
   __device__ __forceinline__ bool next(const UmmaArgs& p, Item* it) {
     if (seg < nseg) {
-      const int64_t t_rel = (e - 1) / p.k0 - seg;
-      const int64_t ts = t_rel * p.k0;
-      const int64_t lo = b > ts ? b : ts;
-      const int64_t hi = e < ts + p.k0 ? e : ts + p.k0;
+      const uint32_t k0 = (uint32_t)p.k0;
+      const uint32_t t_rel = (e - 1) / k0 - (uint32_t)seg;
+      const uint32_t ts = t_rel * k0;
+      const uint32_t lo = b > ts ? b : ts;
+      const uint32_t hi = e < ts + k0 ? e : ts + k0;
       it->tile = p.dp_tiles + (int)t_rel;
       it->kb0 = (int)(lo - ts);
       it->kb1 = (int)(hi - ts);
@@ -343,7 +360,7 @@ struct Sched {
       int order = 0;                                 // pieces of this tile below this one
       if (it->split)
         for (int v = w - 1; v >= 0; --v) {
-          const int64_t vb = sk_begin(p, v), ve = sk_begin(p, v + 1);
+          const uint32_t vb = sk_begin(p, v), ve = sk_begin(p, v + 1);
           if (ve <= ts) break;
           if (ve > vb) ++order;
         }
@@ -364,6 +381,7 @@ struct MmaCtx {
   uint32_t sbase, full0, empty0, tfull0, tempty0, tmem_base;
   int cluster_id, num_clusters;
   uint16_t empty_mask, tfull_mask;   // CTAs whose empty / accumulator-ready barriers a commit feeds
+  long long t_entry;                 // debug trace only
 };
 
 template <int KIND, int CG, int KS, int M2, int N2>
@@ -412,22 +430,24 @@ __device__ __forceinline__ void mma_role(const UmmaArgs& p, const MmaCtx& c) {
   Sched sch(p, c.cluster_id, c.num_clusters);
   Item it;
   int item_no = 0;
-  if (p.trace && elect_one())                                // debug: MMA role set up (item 5, slot 7)
+  if (kTrace && p.trace && elect_one())                                // debug: MMA role set up (item 5, slot 7)
     p.trace[((int64_t)c.cluster_id * kTraceItems + 5) * 8 + 7] = globaltimer();
   __syncwarp();
   while (sch.next(p, &it)) {
     mbar_wait(c.tempty0 + 8u * acc, aphase ^ 1u);
     tc_fence_after();
-    uint64_t* tr = (p.trace && item_no < kTraceItems) ? p.trace + ((int64_t)c.cluster_id * kTraceItems + item_no) * 8 : nullptr;
+    uint64_t* tr = (kTrace && p.trace && item_no < kTraceItems) ? p.trace + ((int64_t)c.cluster_id * kTraceItems + item_no) * 8 : nullptr;
     ++item_no;
-    if (tr && elect_one()) tr[2] = globaltimer();
+    if (kTrace && tr && elect_one()) tr[2] = globaltimer();
     __syncwarp();
     const uint32_t dbase = c.tmem_base + (uint32_t)(acc * p.acc_cols);
     for (int kb = it.kb0; kb < it.kb1; ++kb) {
       mbar_wait(c.full0 + 8u * stage, phase);
       tc_fence_after();
-      if (p.trace && item_no == 1 && kb == it.kb0 && elect_one())   // debug: first stage landed (item 7, slot 7)
+      if (kTrace && p.trace && item_no == 1 && kb == it.kb0 && elect_one()) {  // debug: first stage landed (item 7, slot 7)
         p.trace[((int64_t)c.cluster_id * kTraceItems + 7) * 8 + 7] = globaltimer();
+        trace_cycles(p.trace, c.cluster_id, 4, c.t_entry);
+      }
       __syncwarp();
       // descriptor start field = CTA-window byte address >> 4 (14 bits): the cvta result of a CTA
       // with cluster rank > 0 carries the rank above bit 24, which must not leak into LBO
@@ -452,7 +472,8 @@ __device__ __forceinline__ void mma_role(const UmmaArgs& p, const MmaCtx& c) {
     }
     if (elect_one()) {
       umma_commit<CG>(c.tfull0 + 8u * acc, c.tfull_mask);   // accumulator ready for the epilogue
-      if (tr) tr[3] = globaltimer();
+      if (kTrace && tr) tr[3] = globaltimer();
+      if (kTrace && tr && item_no == 1) trace_cycles(p.trace, c.cluster_id, 5, c.t_entry);
     }
     __syncwarp();
     if (++acc == p.acc_bufs) { acc = 0; aphase ^= 1u; }
@@ -465,7 +486,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
        const __grid_constant__ CUtensorMap tmC, float* __restrict__ C,
        const UmmaArgs p) {
-  constexpr int ELEM = KIND == 0 ? 2 : 4;
   constexpr int UK = KIND == 0 ? 16 : 8;     // UMMA_K
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -492,7 +512,8 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
   const uint16_t all_mask = (uint16_t)((1u << csize) - 1u);
   const uint16_t pair_mask = (uint16_t)(((1u << CG) - 1u) << (pj * CG));
 
-  if (p.trace && warp == 0 && lane == 0 && leader)          // debug: kernel entry (item 0, slot 7)
+  const long long t_entry = (kTrace && p.trace) ? clock64() : 0;
+  if (kTrace && p.trace && warp == 0 && lane == 0 && leader)          // debug: kernel entry (item 0, slot 7)
     p.trace[((int64_t)(blockIdx.x / CG) * kTraceItems) * 8 + 7] = globaltimer();
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
@@ -509,8 +530,10 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
       mbar_init(tempty0 + 8u * b, kEpiWarps * CG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (p.trace && leader)                                   // debug: barriers initialised (item 2, slot 7)
+    if (kTrace && p.trace && leader) {                                 // debug: barriers initialised (item 2, slot 7)
       p.trace[((int64_t)(blockIdx.x / CG) * kTraceItems + 2) * 8 + 7] = globaltimer();
+      trace_cycles(p.trace, blockIdx.x / CG, 0, t_entry);
+    }
   }
   if (warp == 2) {
     if constexpr (CG == 1) {
@@ -520,24 +543,29 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
       asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(p.tmem_cols));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     }
-    if (p.trace && leader && lane == 0)                      // debug: TMEM allocated (item 3, slot 7)
+    if (kTrace && p.trace && leader && lane == 0) {                    // debug: TMEM allocated (item 3, slot 7)
       p.trace[((int64_t)(blockIdx.x / CG) * kTraceItems + 3) * 8 + 7] = globaltimer();
+      trace_cycles(p.trace, blockIdx.x / CG, 1, t_entry);
+    }
   }
   tc_fence_before();
   if (csize > 1) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  if (p.trace && warp == 0 && lane == 0 && leader)          // debug: prologue barrier passed (item 4, slot 7)
+  if (kTrace && p.trace && warp == 0 && lane == 0 && leader) {        // debug: prologue barrier passed (item 4, slot 7)
     p.trace[((int64_t)(blockIdx.x / CG) * kTraceItems + 4) * 8 + 7] = globaltimer();
+    trace_cycles(p.trace, blockIdx.x / CG, 2, t_entry);
+  }
 
+  const int rows_cta = p.m2 * 128;
   const int cluster_id = blockIdx.x / csize;
   const int num_clusters = gridDim.x / csize;
-  const int rows_cta = p.m2 * 128;
 
   if (warp == 0) {
     // ===== TMA producer: the whole warp walks the ring, one elected lane issues =====
     int stage = 0;
     uint32_t phase = 0;
+    constexpr int ELEM = KIND == 0 ? 2 : 4;
     const int kchunks = p.bk * ELEM / p.swz_a;
     const int bboxes = p.nb / p.b_cw;
     const uint32_t bbox_bytes = (uint32_t)(p.bk * p.swz_b);
@@ -554,8 +582,9 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
         mbar_wait(empty0 + 8u * stage, phase ^ 1u);
         const uint32_t fb = full0 + 8u * stage;
         if (elect_one()) {
-          if (p.trace && leader && tp_first) {             // debug: first TMA issued (item 6, slot 7)
+          if (kTrace && p.trace && leader && tp_first) {             // debug: first TMA issued (item 6, slot 7)
             p.trace[((int64_t)cluster_id * kTraceItems + 6) * 8 + 7] = globaltimer();
+            trace_cycles(p.trace, cluster_id, 3, t_entry);
             tp_first = false;
           }
           if (leader) mbar_arrive_expect_tx(fb, p.tx_bytes * CG);
@@ -593,7 +622,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
       // below the 64-128 cycles one MMA occupies the tensor pipe).
       const int code = (p.bk / UK) * 4 + (p.m2 - 1) * 2 + (p.n2 - 1);
       MmaCtx c{sbase, full0, empty0, tfull0, tempty0, tmem_base, cluster_id, num_clusters,
-               (uint16_t)(csize > 1 ? all_mask : 0), (uint16_t)(CG == 2 ? pair_mask : 0)};
+               (uint16_t)(csize > 1 ? all_mask : 0), (uint16_t)(CG == 2 ? pair_mask : 0), t_entry};
       switch (code) {
 #define TT_MMA_CASE(KS, M2, N2) \
   case KS * 4 + (M2 - 1) * 2 + (N2 - 1): mma_role<KIND, CG, KS, M2, N2>(p, c); break;
@@ -625,7 +654,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     Item it;
     int item_no = 0;
     while (sch.next(p, &it)) {
-      uint64_t* tr = (p.trace && warp == 4 && lane == 0 && leader && item_no < kTraceItems)
+      uint64_t* tr = (kTrace && p.trace && warp == 4 && lane == 0 && leader && item_no < kTraceItems)
                          ? p.trace + ((int64_t)cluster_id * kTraceItems + item_no) * 8 : nullptr;
       ++item_no;
       const int tm = it.tile % p.m0, tn = it.tile / p.m0;
@@ -634,7 +663,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
       const bool add = it.split && it.order > 0;           // higher k-blocks: add onto C
       mbar_wait(tfull0 + 8u * acc, aphase);
       tc_fence_after();
-      if (tr) {
+      if (kTrace && tr) {
         tr[0] = (uint64_t)it.tile;
         tr[1] = (uint64_t)it.kb0 | ((uint64_t)it.kb1 << 16) | ((uint64_t)it.order << 32);
         tr[4] = globaltimer();
@@ -643,7 +672,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
         wait_flag(flag, (uint32_t)kEpiWarps * (uint32_t)it.order);   // every epilogue warp of each piece below
         fence_proxy_async_global();
       }
-      if (tr) tr[5] = globaltimer();
+      if (kTrace && tr) tr[5] = globaltimer();
       const int row_cta = tm * (CG * rows_cta) + (int)rank * rows_cta;
       int chunk = 0;                                       // running chunk index over the tile
       for (int mi = 0; mi < p.m2; ++mi) {
@@ -707,9 +736,10 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
           if (it.kb1 == p.k0 && old == (uint32_t)kEpiWarps * ((uint32_t)it.order + 1u) - 1u) *flag = 0u;   // top piece lands last: reset
         }
       }
-      if (tr) {
+      if (kTrace && tr) {
         bulk_wait_all();
         tr[6] = globaltimer();
+        if (item_no == 1) trace_cycles(p.trace, cluster_id, 6, t_entry);
       }
       if (++acc == p.acc_bufs) { acc = 0; aphase ^= 1u; }
     }
@@ -721,8 +751,10 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
   tc_fence_before();
   if (csize > 1) cluster_sync(); else __syncthreads();
   tc_fence_after();
-  if (p.trace && warp == 0 && lane == 0 && leader)          // debug: teardown reached (item 1, slot 7)
+  if (kTrace && p.trace && warp == 0 && lane == 0 && leader) {        // debug: teardown reached (item 1, slot 7)
     p.trace[((int64_t)(blockIdx.x / CG) * kTraceItems + 1) * 8 + 7] = globaltimer();
+    trace_cycles(p.trace, blockIdx.x / CG, 7, t_entry);
+  }
   if (warp == 2) {
     if constexpr (CG == 1)
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(p.tmem_cols));
@@ -941,8 +973,12 @@ void plan_of(const Space& sp, const State& s, Plan* pl) {
                          ((kind == 0 ? 8192.0 : 4096.0) * pl->csize * 1.9e3);
   const double gain_us = (1.0 - (double)rem / P) * tile_us;
   const int mode = tail_split_mode();
+  // the device schedule computes k-block offsets in 32 bits (Sched)
+  const bool fits32 = (uint64_t)P * (uint64_t)tiles * (uint64_t)a.k0 < (1ull << 32);
   const bool worth = tiles - rem >= P && a.acc_bufs == 2 && gain_us >= 8.0;
-  if (mode == 3 && a.k0 >= 2 && tiles * pl->csize <= kFlagWords) {
+  if (!fits32) {
+    pl->grid = std::min(tiles, P) * pl->csize;
+  } else if (mode == 3 && a.k0 >= 2 && tiles * pl->csize <= kFlagWords) {
     // experiment: stream-K over every tile (each cluster gets tiles k0 / P k-blocks)
     a.sk_tiles = tiles;
     a.dp_tiles = 0;
@@ -990,7 +1026,7 @@ tt_status launch_t(const Plan& pl, const CUtensorMap& ma, const CUtensorMap& mb,
     }
     a.flag_group = split_flag_group(stream);
   }
-  static const char* trace_path = std::getenv("TT_UMMA_TRACE");
+  static const char* trace_path = kTrace ? std::getenv("TT_UMMA_TRACE") : nullptr;   // trace build only
   const size_t trace_words = (size_t)(pl.grid / CG) * kTraceItems * 8;
   if (trace_path) {
     if (!cuda_ok(cudaMalloc(&a.trace, trace_words * 8), err, "cudaMalloc(trace)")) return TT_E_CUDA;

@@ -9,7 +9,8 @@ import sys
 
 import numpy as np
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
 
 
 def main():
@@ -21,11 +22,19 @@ def main():
     ap.add_argument("--config", required=True)
     ap.add_argument("--out", default="gpurun_out/umma_trace.bin")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--mhz", type=float, default=1965.0, help="SM clock for cycles -> us")
     ap.add_argument("--flush", action="store_true", help="256 MiB memset before every launch (bench protocol)")
     a = ap.parse_args()
     if os.path.exists(a.out):
         os.remove(a.out)
     os.environ["TT_UMMA_TRACE"] = a.out
+    # the trace instrumentation exists only in the trace build of the library
+    lib = os.path.join(ROOT, "build", "variants", "trace", "libtiletune.so")
+    if not os.path.exists(lib):
+        sys.path.insert(0, ROOT)
+        from paper_1909_10616_b200 import build
+        lib = build.build_variant("trace", ["TT_UMMA_TRACE_BUILD"])
+    os.environ.setdefault("TT_LIB_PATH", lib)
     import torch
     from paper_1909_10616_b200 import tiletune as tt
     fam = {"bf16": tt.FAM_BF16_UMMA, "tf32": tt.FAM_TF32_UMMA}[a.family]
@@ -68,6 +77,16 @@ def main():
             v = v[v > 0]
             if v.size:
                 print(f"  {what}: {(v.min() - t0) / 1e3:.2f} .. {(v.max() - t0) / 1e3:.2f} us")
+        names = ["barriers init", "TMEM alloc", "prologue barrier", "first TMA issue", "first stage landed",
+                 "item 0 last MMA commit", "item 0 epilogue done", "teardown"]
+        cyc = tr[:, 8:16, 7]
+        print("  per-CTA cycles since entry (median over clusters; us at %.0f MHz):" % a.mhz)
+        for i, nm in enumerate(names):
+            v = cyc[:, i]
+            v = v[v > 0]
+            if v.size:
+                print(f"    {nm:24s} {int(np.median(v)):7d} cyc  {np.median(v) / a.mhz:6.2f} us  "
+                      f"(min {v.min() / a.mhz:.2f} max {v.max() / a.mhz:.2f})")
         ends = []
         for c in range(ncl):
             items = []
