@@ -43,7 +43,7 @@ struct Ctx : tt_ctx {
   void *hA = nullptr, *hB = nullptr, *hC = nullptr;
   size_t hAcap = 0, hBcap = 0, hCcap = 0;
   cudaStream_t s_in = nullptr, s_out = nullptr;   // gemm_host copy streams (H2D, D2H)
-  cudaEvent_t e_b = nullptr, e_in[8] = {}, e_c[8] = {};
+  cudaEvent_t e_b = nullptr, e_in[8] = {}, e_c[16] = {};
 
   ~Ctx();
   tt_status init(std::string* err);
