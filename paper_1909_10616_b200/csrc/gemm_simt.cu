@@ -150,12 +150,38 @@ k1_simt(SimtArgs p) {
   const int64_t M = p.M;
   const float* Bb = p.B + (int64_t)blockIdx.x * BN;
 
+  // Strength-reduced slab copies: with power-of-two BK (A) / BN/4 (B) dividing the thread count,
+  // a thread's k (A) or column (B) offset is the same in every iteration and its row advances by
+  // a fixed step, so each cp.async costs two pointer increments instead of a divide / multiply
+  // chain (the copy phase held 16 % of the stall samples at 2048^3, profiles/r11_ncu_k1_simt_2048.md).
+  // Only the 128-accumulator tiles use it: they are register-bound at one occupancy level anyway,
+  // while the smaller tiles' extra live registers cost them occupancy (measured -7 .. -23 % at
+  // 512^3 / 1024^3, +1.4 % / +3.2 % at 2048^3 / 4096^3; profiles/r11_simt_copy_ab.txt).
+  constexpr bool kFastCopy = TM * TN >= 128;
+  const bool a_fast = kFastCopy && !p.a_tn && p.bk_sh >= 0 && (T & (BK - 1)) == 0 && BM % (T >> p.bk_sh) == 0;
+  const int a_rstep = a_fast ? (T >> p.bk_sh) : 1;
+  const int a_c = t & (BK - 1), a_r0 = a_fast ? (t >> p.bk_sh) : 0;
+  const int q4 = BN >> 2;
+  const bool b_fast = kFastCopy && p.b_vec && p.bq_sh >= 0 && (T & (q4 - 1)) == 0 && BK % (T >> p.bq_sh) == 0;
+  const int b_rstep = b_fast ? (T >> p.bq_sh) : 1;
+  const int b_c = (t & (q4 - 1)) << 2, b_r0 = b_fast ? (t >> p.bq_sh) : 0;
+
   auto load = [&](int kt, int buf) {
     float* as = As + buf * BK * LDA;
     float* bs = Bs + buf * BK * LDB;
     const int64_t kb = (int64_t)kt * BK;
     const int na = BM * BK;
-    if (p.a_tn) {                          // W rows are already k-major: As[k][m] needs no transpose
+    if (a_fast) {                          // rows a_r0, a_r0 + a_rstep, ... of column k = kb + a_c
+      const float* src = Ab + (int64_t)a_r0 * K + kb + a_c;
+      float* dst = as + a_c * LDA + a_r0;
+      const int64_t sstep = (int64_t)a_rstep * K;
+#pragma unroll 4
+      for (int r = a_r0; r < BM; r += a_rstep) {
+        cp_async4(dst, src);
+        dst += a_rstep;
+        src += sstep;
+      }
+    } else if (p.a_tn) {                          // W rows are already k-major: As[k][m] needs no transpose
       if (p.a_vec16) {
         const int q = BM >> 2;
         for (int e = t; e < BK * q; e += T) {
@@ -179,7 +205,18 @@ k1_simt(SimtArgs p) {
         cp_async4(as + c * LDA + r, Ab + (int64_t)r * K + kb + c);
       }
     }
-    if (p.b_vec) {
+    if (b_fast) {                          // rows b_r0, b_r0 + b_rstep, ... of 16-byte column b_c
+      const float* src = Bb + (kb + b_r0) * N + b_c;
+      float* dst = bs + b_r0 * LDB + b_c;
+      const int64_t sstep = (int64_t)b_rstep * N;
+      const int dstep = b_rstep * LDB;
+#pragma unroll 4
+      for (int r = b_r0; r < BK; r += b_rstep) {
+        cp_async16(dst, src);
+        dst += dstep;
+        src += sstep;
+      }
+    } else if (p.b_vec) {
       const int q = BN >> 2;
       const int nb = BK * q;
       if (p.bq_sh >= 0) {
