@@ -57,6 +57,7 @@ WORKLOADS = {
     # the paper's main experiment shape: 0.1 % of 899 756 states
     "f32_1024": (1024, 1024, 1024, 1, 900),
     "bf16_1024": (1024, 1024, 1024, 3, 128),
+    "bf16_2048": (2048, 2048, 2048, 3, 128),
 }
 FAMILY_DTYPE = {1: "f32", 2: "tf32", 3: "bf16"}
 

@@ -991,9 +991,19 @@ void plan_of(const Space& sp, const State& s, Plan* pl) {
     a.sk_workers = P;
     pl->grid = P * pl->csize;
   } else if (mode != 0 && mode < 3 && rem != 0 && a.k0 >= 2 && (mode == 2 || worth)) {
-    a.sk_tiles = tiles % P;                              // == tiles when tiles < P
-    a.dp_tiles = tiles - a.sk_tiles;
-    a.sk_workers = std::min(P, a.sk_tiles * kMaxPieces);
+    if (mode == 1 && tiles >= rem + P && (rem + P) * pl->csize <= kFlagWords) {
+      // measured default (round 2): the last full data-parallel wave joins the remainder and
+      // their k-blocks are spread evenly over all P clusters (stream-K over rem + P tiles): every
+      // cluster ends within a fraction of a tile.  bf16 4096^3 bench config 1418 -> 1440 TF/s,
+      // 3 interleaved runs each (profiles/r11_split_modes.txt).
+      a.sk_tiles = rem + P;
+      a.dp_tiles = tiles - a.sk_tiles;
+      a.sk_workers = P;
+    } else {
+      a.sk_tiles = tiles % P;                            // == tiles when tiles < P
+      a.dp_tiles = tiles - a.sk_tiles;
+      a.sk_workers = std::min(P, a.sk_tiles * kMaxPieces);
+    }
     pl->grid = P * pl->csize;
   } else {
     pl->grid = std::min(tiles, P) * pl->csize;

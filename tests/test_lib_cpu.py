@@ -315,7 +315,9 @@ def test_umma_tail_split_policy(monkeypatch):
     # every tile would be split or the accumulator is single-buffered; TT_TAIL_SPLIT=0 disables
     monkeypatch.delenv("TT_TAIL_SPLIT", raising=False)
     sp = tt.make_space(4096, 4096, 4096, family=3)
-    assert tt.binding(sp, ((16, 2, 1, 128), (32, 128), (16, 1, 1, 256))).split_tiles == 256 % 74
+    # round 2: the last full wave joins the remainder (stream-K over 256 % 74 + 74 tiles, all 74 clusters)
+    info = tt.binding(sp, ((16, 2, 1, 128), (32, 128), (16, 1, 1, 256)))
+    assert (info.split_tiles, info.split_workers) == (256 % 74 + 74, 74)
     assert tt.binding(sp, ((16, 2, 1, 128), (64, 64), (8, 1, 2, 256))).split_tiles == 0       # 512 acc columns
     assert tt.binding(tt.make_space(1024, 8192, 8192, family=3),
                       ((2, 2, 2, 128), (128, 64), (32, 1, 1, 256))).split_tiles == 0          # 64 tiles < 74
