@@ -238,9 +238,9 @@ def tune(ctx, sp, Mr, N, K, fam, layout, budget, args, world, coll, local):
     sopts = tt.search_opts(family=fam, seed=args.seed, width=args.width, layout=layout,
                            measure={"l2_flush": 1 if args.tune_l2_flush else 0})
     ms_fn, observe, cut_fn = tdist.device_measure_set(ctx, sp, sopts, device=local)
-    store = tdist.default_store() if (world > 1 and args.assign == "dynamic") else None
+    store = tdist.default_store() if (world > 1 and args.assign in ("dynamic", "auto")) else None
     ev = tdist.TrackingEvaluator(observe=observe, measure_set=ms_fn, device=coll if world > 1 else None,
-                                 store=store, assign="lpt" if (args.assign == "dynamic" and store is None) else args.assign,
+                                 store=store, assign="lpt" if (args.assign in ("dynamic", "auto") and store is None) else args.assign,
                                  space=sp, cut_s=cut_fn)
     ctx.prepare(sp)                      # one-time setup (operands, flush buffer, kernels loaded) off the clock
     if world > 1:
@@ -284,14 +284,19 @@ def tune(ctx, sp, Mr, N, K, fam, layout, budget, args, world, coll, local):
             wl = host + tdist.projected_sharded_wall(ev.round_times, G, weights=ev.round_weights, **kw)
             wd = host + tdist.projected_sharded_wall(ev.round_times, G, dynamic=True, per_claim_s=200e-6,
                                                      weights=ev.round_weights, **kw)
-            proj[str(G)] = {"dynamic_wall_s": wd, "dynamic_speedup": tune_wall / wd if wd > 0 else None,
+            wa = host + tdist.projected_sharded_wall(ev.round_times, G, auto=True, per_claim_s=200e-6,
+                                                     weights=ev.round_weights, **kw)
+            proj[str(G)] = {"auto_wall_s": wa, "auto_speedup": tune_wall / wa if wa > 0 else None,
+                            "dynamic_wall_s": wd, "dynamic_speedup": tune_wall / wd if wd > 0 else None,
                             "lpt_wall_s": wl, "lpt_speedup": tune_wall / wl if wl > 0 else None,
                             "static_wall_s": ws, "static_speedup": tune_wall / ws if ws > 0 else None}
         rec["projected_sharded_search"] = {"rounds": ev.rounds, "round_sizes": [len(t) for t in ev.round_times],
                                            "measure_s": meas, "host_s": host, "by_gpus": proj,
                                            "model": "round by round: slowest rank's measurement time + 50 us exchange; "
-                                                    "dynamic = claims in LPT order (200 us each); round 0 speculates "
-                                                    "g(s0) on the idle ranks; host search work replicated",
+                                                    "dynamic = claims in LPT order (200 us each); auto (the N > 1 "
+                                                    "default) = dynamic in rounds whose median predicted candidate "
+                                                    "time is >= 2 ms, else LPT; round 0 speculates g(s0) on the idle "
+                                                    "ranks; host search work replicated",
                                            "kind": "projection from 1-GPU per-candidate times"}
     return res.best, rec
 
@@ -412,7 +417,7 @@ def main():
     ap.add_argument("--budget", type=int, default=None, help="G-BFS evaluation budget (distinct configs)")
     ap.add_argument("--width", type=int, default=16,
                     help="G-BFS states popped per round W (reading Z9): the same for every GPU count")
-    ap.add_argument("--assign", choices=["lpt", "static", "dynamic"], default="dynamic",
+    ap.add_argument("--assign", choices=["auto", "lpt", "static", "dynamic"], default="auto",
                     help="how a round's candidates are spread over the ranks (paper_1909_10616_b200/dist.py)")
     ap.add_argument("--layout", choices=["nn", "tn"], default="nn",
                     help="tn: A stored as W[K][M] (the paper's perceptron Y = W^T X, P:372)")

@@ -28,6 +28,19 @@ from . import tiletune as tt
 # probe costs one launch, a full one ~11 (cold probe, 10 repeats), plus host overhead
 _FULL_LAUNCHES = 11
 _PER_CANDIDATE_S = 2e-3
+# one dynamic claim (a TCPStore add round trip); "auto" claims dynamically only in rounds whose
+# median predicted measurement time is >= _AUTO_CLAIMS claims, else it uses the LPT plan
+_CLAIM_S = 200e-6
+_AUTO_CLAIMS = 10
+
+
+def auto_mode(weights: Sequence[float]) -> str:
+    """The "auto" rule for one round (identical on every rank: the weights come from the
+    replicated known costs): dynamic claiming when the median predicted measurement time is at
+    least _AUTO_CLAIMS claim round trips, else the LPT plan (no per-candidate store traffic)."""
+    raw = sorted(w - _PER_CANDIDATE_S for w in weights)
+    med = raw[len(raw) // 2] if raw else 0.0
+    return "dynamic" if med >= _AUTO_CLAIMS * _CLAIM_S else "lpt"
 
 
 class ShardedEvaluator:
@@ -47,6 +60,10 @@ class ShardedEvaluator:
     * ``"static"``: candidate j on rank j mod G.
     * ``"dynamic"`` (``store`` given): ranks claim the next unmeasured candidate, in the LPT
       order of the predictions, from a shared counter (``store.add``) whenever they are free.
+    * ``"auto"`` (``store`` given): per round, dynamic when the median predicted measurement time
+      is at least 10 claim round trips (~2 ms), else the LPT plan -- short candidates (bf16 at
+      4096^3, ~1 ms each) do not pay a store round trip apiece, long ones (fp32) balance
+      dynamically.
 
     Speculation (``speculate``, needs ``space``): in round 0 -- s0 alone, so G - 1 ranks would
     idle -- the idle ranks measure s0's neighbourhood g(s0), from which round 1 draws all of its
@@ -83,9 +100,13 @@ class ShardedEvaluator:
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.device = device or torch.device("cpu")
         self.store = store if self.world > 1 else None
-        self.assign = "dynamic" if self.store is not None else (assign or "lpt")
+        if assign == "auto":
+            self.assign = "auto" if self.store is not None else "lpt"
+        else:
+            self.assign = "dynamic" if self.store is not None else (assign or "lpt")
         if self.assign == "dynamic" and self.store is None and self.world > 1:
             raise ValueError("dynamic assignment needs a store")
+        self.round_modes: List[str] = []
         self.space = space
         self.cut_s = cut_s
         self.ns = f"tt_eval{next(ShardedEvaluator._instances)}"
@@ -180,11 +201,13 @@ class ShardedEvaluator:
         todo = [j for j in range(n) if not hit[j]]
         sub = [states[j] for j in todo]
         m = len(sub)
-        wts = self.weights(sub) if self.assign in ("lpt", "dynamic") else [1.0] * m
+        wts = self.weights(sub) if self.assign in ("lpt", "dynamic", "auto") else [1.0] * m
+        mode = auto_mode(wts) if self.assign == "auto" else self.assign
+        self.round_modes.append(mode)
         spec = self._speculative(sub)
         S = len(spec)
         vals = [0.0] * (2 * m + 2 * S)          # costs, seconds (this round), then speculative costs, seconds
-        if self.assign == "dynamic" and self.world > 1:
+        if mode == "dynamic" and self.world > 1:
             # claim in longest-predicted-first order (LPT order) from a shared counter
             order = sorted(range(m), key=lambda j: (-wts[j], j))
             key = f"{self.ns}_round{self.rounds}"
@@ -205,7 +228,7 @@ class ShardedEvaluator:
                     vals[2 * m + q], vals[2 * m + S + q] = c[q], t[q]
             spec_owner = []
         else:
-            if self.assign == "lpt":
+            if mode == "lpt":
                 owner = self.lpt_owners(wts, self.world)
             else:
                 owner = [j % self.world for j in range(m)]
@@ -230,7 +253,7 @@ class ShardedEvaluator:
             buf = torch.tensor(vals, dtype=torch.float64, device=self.device)
             dist.all_reduce(buf, op=dist.ReduceOp.MAX, group=self.group)
             vals = buf.cpu().tolist()
-            if self.assign == "dynamic" and self.rank == 0:
+            if mode == "dynamic" and self.rank == 0:
                 for k in (f"{self.ns}_round{self.rounds}", f"{self.ns}_round{self.rounds}_spec"):
                     try:                                 # every rank has left its claim loops
                         self.store.delete_key(k)
@@ -308,7 +331,8 @@ def _busy(times: Sequence[float], world: int, mode: str, weights: Optional[Seque
 def projected_sharded_wall(round_times: Sequence[Sequence[float]], world: int, per_round_s: float = 0.0,
                            dynamic: bool = False, per_claim_s: float = 0.0,
                            weights: Optional[Sequence[Sequence[float]]] = None,
-                           states: Optional[Sequence[Sequence]] = None, neighbors: Optional[Callable] = None) -> float:
+                           states: Optional[Sequence[Sequence]] = None, neighbors: Optional[Callable] = None,
+                           auto: bool = False) -> float:
     """Measurement wall time of the same traversal sharded over ``world`` ranks, from
     per-candidate times recorded on one rank: sum over rounds of the slowest rank's busy time,
     plus ``per_round_s`` (the exchange) per round.  Static: candidate j on rank j mod world.
@@ -317,9 +341,12 @@ def projected_sharded_wall(round_times: Sequence[Sequence[float]], world: int, p
     free first, each claim costing ``per_claim_s``.  ``states`` + ``neighbors`` given: the
     speculative round 0 (ShardedEvaluator.speculate) -- the idle ranks measure g(s0) while s0 runs,
     each such state costing what it cost when the search measured it (else the dearest of them),
-    and later rounds do not re-measure those states.  A projection from measured times, not a
-    multi-GPU measurement."""
+    and later rounds do not re-measure those states.  ``auto`` (needs ``weights``): each round
+    dynamic or LPT by the evaluator's auto rule (``auto_mode``).  A projection from measured
+    times, not a multi-GPU measurement."""
     mode = "dynamic" if dynamic else ("lpt" if weights is not None else "static")
+    if auto:
+        mode = "auto"
     spec_t = {}
     if states is not None and neighbors is not None and world > 1 and round_times and len(round_times[0]) < world:
         seen = set(states[0])
@@ -345,10 +372,11 @@ def projected_sharded_wall(round_times: Sequence[Sequence[float]], world: int, p
             w = [w[j] for j in keep] if w is not None else None
             for s in states[k]:                            # a speculative state is served once
                 spec_t.pop(s, None)
-        busy = _busy(times, world, mode, w, per_claim_s)
+        rmode = (auto_mode(weights[k]) if weights is not None else "static") if mode == "auto" else mode
+        busy = _busy(times, world, rmode, w, per_claim_s)
         if spec_t and k == 0:
             st = list(spec_t.values())
-            if mode == "dynamic":
+            if rmode == "dynamic":
                 for t in st:
                     r = min(range(world), key=lambda i: busy[i])
                     busy[r] += t + per_claim_s

@@ -36,13 +36,17 @@ def _worker(rank, world, port, algo, out, mode="static"):
         measured.append(s)
         return costs.t2_cost(sp, s)
 
+    if mode == "auto_dyn":                  # auto with every round long enough to claim dynamically
+        tdist._AUTO_CLAIMS = 0
+    amode = "auto" if mode.startswith("auto") else mode
+
     def make():
-        return tdist.ShardedEvaluator(measure_one, store=tdist.default_store() if mode == "dynamic" else None,
-                                      assign=mode if mode != "dynamic" else None,
-                                      space=tt.make_space(64, 64, 64) if mode == "lpt" else None)
+        return tdist.ShardedEvaluator(measure_one, store=tdist.default_store() if amode in ("dynamic", "auto") else None,
+                                      assign=amode if amode != "dynamic" else None,
+                                      space=tt.make_space(64, 64, 64) if amode in ("lpt", "auto") else None)
 
     ev = make()
-    assert ev.assign == mode
+    assert ev.assign == amode
     if algo == "gbfs":
         res = tt.gbfs_search(64, 64, 64, 300, tt.search_opts(seed=4, width=8), batch=ev)
     else:
@@ -54,12 +58,13 @@ def _worker(rank, world, port, algo, out, mode="static"):
     row_ranges = tdist.row_shard(8192, world, rank)
     out[rank] = ([(r["state"], r["cost"]) for r in res.trace], n_first, ev.rounds, row_ranges,
                  [(r["state"], r["cost"]) for r in res2.trace], len(measured) - n_first,
-                 (ev.spec_measured, ev.spec_used, ev2.spec_measured, ev2.spec_used))
+                 (ev.spec_measured, ev.spec_used, ev2.spec_measured, ev2.spec_used), sorted(set(ev.round_modes)))
     dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("algo,mode", [("gbfs", "static"), ("na2c", "static"), ("gbfs", "dynamic"),
-                                       ("na2c", "dynamic"), ("gbfs", "lpt"), ("na2c", "lpt")])
+                                       ("na2c", "dynamic"), ("gbfs", "lpt"), ("na2c", "lpt"),
+                                       ("gbfs", "auto"), ("gbfs", "auto_dyn")])
 def test_sharded_search_matches_oracle(algo, mode):
     world = 2
     mgr = mp.Manager()
@@ -72,11 +77,14 @@ def test_sharded_search_matches_oracle(algo, mode):
     else:
         o = ona2c.na2c(sp, ogbfs.table_source(sp, tab), budget=200, params=ona2c.Params(epsilon=0.0), seed=4)
     ref = [(r.state, r.cost) for r in o.trace]
-    t0, n0, rounds0, rr0, u0, m0, sp0 = out[0]
-    t1, n1, rounds1, rr1, u1, m1, sp1 = out[1]
+    t0, n0, rounds0, rr0, u0, m0, sp0, md0 = out[0]
+    t1, n1, rounds1, rr1, u1, m1, sp1, md1 = out[1]
+    assert md0 == md1                                      # every rank took the same per-round modes
+    if mode == "auto_dyn":
+        assert md0 == ["dynamic"]
     assert t0 == t1 == ref                                 # identical traversal on every rank = oracle
     assert sp0 == sp1                                      # every rank agrees on the speculation
-    if mode == "lpt":                                      # g(s0) measured while s0 runs (1 idle rank)
+    if mode in ("lpt", "auto", "auto_dyn"):                # g(s0) measured while s0 runs (1 idle rank)
         assert sp0[0] == len(space.neighbors(sp, space.initial_state(sp))) and 5 <= sp0[1] <= sp0[0]
     else:
         assert sp0 == (0, 0, 0, 0)
@@ -134,3 +142,17 @@ def test_predicted_cost_equals_min_over_legit_neighbors():
             want = min(nb) if nb else min(ev.known.values())
             assert ev._predicted_cost(s) == want
             assert set(tt.neighbors(sp, s)) <= set(ev._moves(s))
+
+
+def test_auto_mode_and_projection():
+    # auto: dynamic claims only when the median predicted measurement time is >= 10 claims (2 ms)
+    short = [tdist._PER_CANDIDATE_S + 1e-3] * 5
+    long_ = [tdist._PER_CANDIDATE_S + 5e-3] * 5
+    assert tdist.auto_mode(short) == "lpt" and tdist.auto_mode(long_) == "dynamic"
+    rt = [[4.0, 1.0, 1.0, 1.0, 1.0]]
+    # a round of short predictions projects exactly like LPT, a round of long ones like dynamic
+    w_short = [[tdist._PER_CANDIDATE_S + x * 1e-4 for x in (4, 1, 1, 1, 1)]]
+    w_long = [[tdist._PER_CANDIDATE_S + x * 1e-2 for x in (4, 1, 1, 1, 1)]]
+    for w, kw in ((w_short, {}), (w_long, {"dynamic": True})):
+        assert tdist.projected_sharded_wall(rt, 2, auto=True, per_claim_s=0.1, weights=w) == \
+            tdist.projected_sharded_wall(rt, 2, per_claim_s=0.1, weights=w, **kw)

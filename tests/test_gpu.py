@@ -231,6 +231,41 @@ def test_umma_tail_split(fam, cfg, monkeypatch):
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
 
 
+@pytest.mark.parametrize("fam,cfg", [
+    (3, ((16, 1, 1, 128), (8, 64), (16, 1, 1, 128))),     # 256 tiles, 148 clusters: 108 + 148 split
+    (3, ((8, 2, 1, 128), (8, 64), (16, 1, 1, 128))),      # 128 pair tiles on 74 pairs: all stream-K
+    (3, ((16, 1, 1, 128), (8, 64), (16, 2, 1, 64))),      # n1 = 2 clusters (A multicast): 34 + 74 split
+    (2, ((16, 1, 1, 128), (16, 32), (16, 1, 1, 128))),    # tf32
+])
+def test_umma_wave_remainder_split(fam, cfg, monkeypatch):
+    # Round-2 default split shape: the last full wave plus the remainder by
+    # stream-K over all clusters.  TT_TAIL_SPLIT=4 forces it at this small K; parity vs the double
+    # oracle, bit-reproducible across launches and streams.
+    monkeypatch.setenv("TT_TAIL_SPLIT", "4")
+    M = N = 2048
+    K = 512
+    sp = tt.make_space(M, N, K, family=fam)
+    info = tt.binding(sp, cfg)
+    tiles = cfg[0][0] * cfg[2][0]
+    assert info.split_tiles > 0 and info.split_tiles == tiles % info.split_workers + info.split_workers
+    bf16 = fam == tt.FAM_BF16_UMMA
+    A, B = host_inputs(M, N, K, bf16=bf16)
+    R = og.gemm_f64(A, B)
+    Ad, Bd = to_dev(A, bf16), to_dev(B, bf16)
+    outs = []
+    s2 = torch.cuda.Stream()
+    for stream in (None, None, s2):
+        C = torch.full((M, N), float("nan"), device=DEV)
+        if stream is None:
+            tt.gemm(Ad, Bd, C, fam, cfg)
+        else:
+            with torch.cuda.stream(stream):
+                tt.gemm(Ad, Bd, C, fam, cfg, stream=stream)
+        torch.cuda.synchronize()
+        outs.append(C.cpu().numpy())
+    assert og.normwise_error(outs[0], R) <= 5e-3
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
 
 # ------------------------------------------------------------------ evaluator and search
 def test_measure_and_errors():

@@ -42,6 +42,19 @@ for cfg in [((2, 2, 1, 128), (4, 128), (1, 2, 1, 256)), ((4, 1, 1, 128), (4, 128
     torch.cuda.synchronize()
     ref = A.float() @ B.float()
     print("multicast", cfg, float((C - ref).abs().max() / ref.abs().max()))
+# round 2 default split shape: the last full wave + remainder by stream-K (forced at small sizes)
+os.environ["TT_TAIL_SPLIT"] = "4"
+for fam, M, N, K, cfg in [(3, 2048, 4096, 256, ((8, 2, 1, 128), (2, 128), (16, 1, 1, 256))),
+                          (3, 2048, 2048, 256, ((16, 1, 1, 128), (4, 64), (32, 1, 1, 64)))]:
+    A = torch.randn(M, K, device=dev).to(torch.bfloat16)
+    B = torch.randn(K, N, device=dev).to(torch.bfloat16)
+    C = torch.empty(M, N, device=dev)
+    info = tt.binding(tt.make_space(M, N, K, family=fam), cfg)
+    for _ in range(2):
+        tt.gemm(A, B, C, fam, cfg)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float()
+    print("wave+remainder split", info.split_tiles, info.split_workers, cfg, float((C - ref).abs().max() / ref.abs().max()))
 del os.environ["TT_TAIL_SPLIT"]
 ctx = tt.Context(0)
 smp = ctx.measure(tt.make_space(512, 512, 512, family=3), ((4, 1, 1, 128), (8, 64), (4, 1, 1, 128)),
