@@ -103,10 +103,35 @@ def main():
                   "ends is not counted by the kernel's DRAM counters."]
     with open(os.path.join(PROF, f"{tag}_ncu_k_umma.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
-    with open(os.path.join(PROF, f"traffic_{workload}.json"), "w") as f:
-        json.dump({"config": [cfg["m"], cfg["k"], cfg["n"]], "dram_bytes_per_launch": dram,
-                   "source": f"profiles/{tag}_ncu_k_umma.md"}, f, indent=1)
+    merge_traffic(tag, workload, [cfg["m"], cfg["k"], cfg["n"]])
     print("wrote", tag)
+
+
+def merge_traffic(tag, workload, cfg):
+    """Update the bench config's entry of profiles/traffic_<workload>.json (the table bench.py's
+    roofline.traffic reads) from gpurun_out/traffic_<tag>.csv (ncu --metrics dram bytes of one
+    launch of that config under the current build)."""
+    path = os.path.join(OUT, f"traffic_{tag}.csv")
+    if not os.path.exists(path):
+        return
+    with open(path) as f:
+        lines = [ln for ln in f if ln.startswith('"')]
+    vals = {}
+    for r in csv.DictReader(lines):
+        x = float(r["Metric Value"].replace(",", ""))
+        x *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3, "msecond": 1e6}.get(
+            r.get("Metric Unit", ""), 1)
+        vals[r["Metric Name"]] = x
+    entry = {"config": cfg, "dram_bytes_per_launch": vals.get("dram__bytes_read.sum", 0) + vals.get("dram__bytes_write.sum", 0),
+             "dram_read": vals.get("dram__bytes_read.sum"), "dram_write": vals.get("dram__bytes_write.sum"),
+             "lts_bytes": vals.get("lts__t_bytes.sum"), "ncu_duration_ns": vals.get("gpu__time_duration.sum"),
+             "captured": f"{tag} (tools/gpu_r11_final.sh, current split policy)"}
+    tp = os.path.join(PROF, f"traffic_{workload}.json")
+    table = json.load(open(tp)) if os.path.exists(tp) else {"workload": workload, "configs": []}
+    table.setdefault("configs", [])
+    table["configs"] = [e for e in table["configs"] if e.get("config") != cfg] + [entry]
+    with open(tp, "w") as f:
+        json.dump(table, f, indent=1)
 
 
 if __name__ == "__main__":
