@@ -255,72 +255,14 @@ k1_simt(SimtArgs p) {
     }
   }
 
-#ifdef TT_SIMT_SPREAD
-  constexpr bool kSpread = kFastCopy;
-#else
-  constexpr bool kSpread = false;
-#endif
-  bool spread_done = false;
-  if constexpr (kSpread) {
-    if (a_fast && b_fast && NS == 2) {
-      // Experiment: slab kt+1's copies are issued a few at a time between the FFMA2 blocks of the
-      // first half of slab kt's k-steps instead of in one burst before them, so the copy issue
-      // (15 % of the stall samples at 2048^3) hides in the FFMA2 pipe's free issue slots.
-      load(0, 0);
-      cp_async_commit();
-      const int na_it = BM / a_rstep, nb_it = BK / b_rstep;   // copies per thread per slab
-      const int H = BK / 4 > 0 ? BK / 4 : 1;                  // pair iterations to spread over
-      const int ca = (na_it + H - 1) / H, cb = (nb_it + H - 1) / H;
-      const int64_t sastep = (int64_t)a_rstep * K, sbstep = (int64_t)b_rstep * N;
-      const int dbstep = b_rstep * LDB;
-      int buf = 0;
-      for (int kt = 0; kt < p.k0; ++kt) {
-        cp_async_wait<0>();
-        __syncthreads();
-        const int64_t kb = (int64_t)(kt + 1) * BK;
-        const float* sa = Ab + (int64_t)a_r0 * K + kb + a_c;
-        float* da = As + (buf ^ 1) * BK * LDA + a_c * LDA + a_r0;
-        const float* sb = Bb + (kb + b_r0) * N + b_c;
-        float* db = Bs + (buf ^ 1) * BK * LDB + b_r0 * LDB + b_c;
-        int ra = kt + 1 < p.k0 ? 0 : na_it, rb = kt + 1 < p.k0 ? 0 : nb_it;
-        const float* as = As + buf * BK * LDA + row0;
-        const float* bs = Bs + buf * BK * LDB + col0;
-        float a0[TM], b0[TN], a1[TM], b1[TN];
-        load_frag<TM, TN, kVecA>(as, bs, 0, LDA, LDB, SA, SB, a0, b0);
-        int kk = 0;
-        for (; kk + 2 <= BK; kk += 2) {
-          load_frag<TM, TN, kVecA>(as, bs, kk + 1, LDA, LDB, SA, SB, a1, b1);
-          fma_frag<TM, TN, kPair>(a0, b0, acc, acc2);
-          for (int q = 0; q < ca && ra < na_it; ++q, ++ra) {
-            cp_async4(da, sa);
-            da += a_rstep;
-            sa += sastep;
-          }
-          for (int q = 0; q < cb && rb < nb_it; ++q, ++rb) {
-            cp_async16(db, sb);
-            db += dbstep;
-            sb += sbstep;
-          }
-          if (kk + 2 < BK) load_frag<TM, TN, kVecA>(as, bs, kk + 2, LDA, LDB, SA, SB, a0, b0);
-          fma_frag<TM, TN, kPair>(a1, b1, acc, acc2);
-        }
-        if (kk < BK) fma_frag<TM, TN, kPair>(a0, b0, acc, acc2);
-        cp_async_commit();
-        buf ^= 1;
-        __syncthreads();
-      }
-      spread_done = true;
-    }
-  }
   // prologue: slots 0 .. NS-2 in flight; every iteration commits one group (possibly empty) so
   // wait_group<NS-1> always means "tile kt has landed"
-  if (!spread_done)
   for (int pk = 0; pk < NS - 1; ++pk) {
     if (pk < p.k0) load(pk, pk);
     cp_async_commit();
   }
   int buf = 0;
-  for (int kt = 0; kt < (spread_done ? 0 : p.k0); ++kt) {
+  for (int kt = 0; kt < p.k0; ++kt) {
     const int nxt = kt + NS - 1;
     if (nxt < p.k0) load(nxt, nxt % NS);
     cp_async_commit();
