@@ -363,18 +363,24 @@ def peak_of(fam, peaks, peak_src, sm_max_mhz):
     return (fp32_fma_peak_tflops(smx), f"fp32 FFMA: 148 SM x 128 lanes x 2 x {smx:.0f} MHz (DESIGN.md §6)", "alu")
 
 
-def traffic_of(workload, best):
-    """DRAM bytes per launch of this config from the committed ncu captures, or None."""
+def traffic_entry(workload, best):
+    """The committed ncu record of this config (DRAM bytes per launch, and for the bench config the
+    SM clock and tensor-pipe activity ncu saw inside the kernel), or {}."""
     tp = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
     if not os.path.exists(tp):
-        return None
+        return {}
     with open(tp) as f:
         tr = json.load(f)
     want = [list(v) for v in best]
     for e in tr.get("configs", [tr]):
         if e.get("config") == want:
-            return e.get("dram_bytes_per_launch")
-    return None
+            return e
+    return {}
+
+
+def traffic_of(workload, best):
+    """DRAM bytes per launch of this config from the committed ncu captures, or None."""
+    return traffic_entry(workload, best).get("dram_bytes_per_launch")
 
 
 def fp32_record(ctx, args, world, coll, local, dev, peaks, peak_src, sm_max):
@@ -566,7 +572,11 @@ def main():
             "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": "tt_gemm_host (pinned host A,B -> device -> C host)"},
             "gpu_launches": args.steps,
-            "clocks": clocks,
+            "clocks": dict(clocks, **({"kernel_sm_ghz_ncu": traffic_entry(args.workload, best)["sm_clock_ghz_ncu"],
+                                        "note": "NVML samples every 2 ms land mostly between the ~0.1 ms launches "
+                                                "(flush gaps); kernel_sm_ghz_ncu is the clock ncu measured inside "
+                                                "one launch of this config (profiles/traffic_*.json)"}
+                                       if traffic_entry(args.workload, best).get("sm_clock_ghz_ncu") else {})),
             "spot_check_err": spot_err,
             "per_step_ms": {"min": min(per), "median": statistics.median(per), "max": max(per)},
         }
