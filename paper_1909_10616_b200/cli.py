@@ -145,16 +145,21 @@ def _run(strategy, args, seed, ctx):
         mo = tt.measure_opts(repeats=args.repeats, warmup=args.warmup)
         cache = args._cost_cache
         equiv = [0.0]
+        best = [float("inf")]
 
         def cached(states):
             out = []
             for s in states:
                 if s not in cache:
                     t0 = time.perf_counter()
-                    c = ctx.measure(sp, s, mo).cost_s
+                    # --scoring: the searches' own scoring rules at this search's incumbent (slow
+                    # cut, racing, partial-grid probe; reading Z12), as the DEVICE source applies them
+                    m = tt.scoring_opts(sp, opts, best[0], args.device) if args.scoring else mo
+                    c = ctx.measure(sp, s, m).cost_s
                     cache[s] = (c, time.perf_counter() - t0)
                 out.append(cache[s][0])
                 equiv[0] += cache[s][1]
+                best[0] = min(best[0], cache[s][0])
             return out
         res = fn(args.m, args.n, args.k, args.max_evals, opts, batch=cached)
         res.equiv_wall_s = equiv[0]
@@ -300,6 +305,8 @@ def main(argv=None):
         p.add_argument("--start-config", default=None)
         p.add_argument("--out", default="runs/tune")
         p.add_argument("--resume", default=None, help="CSV trace of an earlier run: replay it, then continue")
+        p.add_argument("--scoring", action="store_true",
+                       help="shared-cache measurements use the searches' scoring rules (cut, racing; reading Z12)")
         p.add_argument("--shared-cache", action="store_true",
                        help="device: measure each distinct state once for the whole run (common measurements)")
         p.set_defaults(fn=fn)
