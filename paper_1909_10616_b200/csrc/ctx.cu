@@ -8,6 +8,9 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include <algorithm>
 #include <cmath>
 #include <map>
@@ -486,6 +489,17 @@ tt_status Ctx::gemm_host(const Space& sp, const State& s, const void* Ah, const 
       }
       std::vector<bool> haveA(R, false), haveB(Q, false);
       int blk = 0;
+      // debug (TT_HOST_TRACE=1): timing events after every copy / GEMM, printed to stderr
+      static const bool trace = std::getenv("TT_HOST_TRACE") != nullptr;
+      std::vector<std::pair<std::string, cudaEvent_t>> tev;
+      auto mark = [&](const std::string& what, cudaStream_t st) {
+        if (!trace) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        tev.push_back({what, e});
+      };
+      mark("start", s_in);
       for (auto [which, t] : order) {
         if (which == 0) {
           if (!cuda_ok(cudaMemcpyAsync(static_cast<char*>(hA) + (size_t)t * Mc * K * es,
@@ -493,6 +507,7 @@ tt_status Ctx::gemm_host(const Space& sp, const State& s, const void* Ah, const 
                                        cudaMemcpyHostToDevice, s_in), err, "H2D A panel"))
             return TT_E_CUDA;
           cudaEventRecord(e_in[t], s_in);
+          mark("H2D A" + std::to_string(t), s_in);
           haveA[t] = true;
         } else {
           if (!cuda_ok(cudaMemcpy2DAsync(static_cast<char*>(hB) + (size_t)t * K * Nc * es, (size_t)Nc * es,
@@ -500,6 +515,7 @@ tt_status Ctx::gemm_host(const Space& sp, const State& s, const void* Ah, const 
                                          (size_t)Nc * es, (size_t)K, cudaMemcpyHostToDevice, s_in), err, "H2D B panel"))
             return TT_E_CUDA;
           cudaEventRecord(e_in[4 + t], s_in);
+          mark("H2D B" + std::to_string(t), s_in);
           haveB[t] = true;
         }
         // every block that this panel completes: (t, j) for landed B_j, or (i, t) for landed A_i
@@ -514,14 +530,26 @@ tt_status Ctx::gemm_host(const Space& sp, const State& s, const void* Ah, const 
           tt_status st = launch_gemm(spb, sb, dA, dB, dC, stream, err);
           if (st != TT_OK) return st;
           cudaEventRecord(e_c[blk], stream);
+          mark("GEMM C" + std::to_string(i) + std::to_string(j), stream);
           cudaStreamWaitEvent(s_out, e_c[blk], 0);
           ++blk;
           if (!cuda_ok(cudaMemcpy2DAsync(Ch + (size_t)i * Mc * N + (size_t)j * Nc, (size_t)N * 4, dC, (size_t)Nc * 4,
                                          (size_t)Nc * 4, (size_t)Mc, cudaMemcpyDeviceToHost, s_out), err, "D2H C block"))
             return TT_E_CUDA;
+          mark("D2H C" + std::to_string(i) + std::to_string(j), s_out);
         }
       }
-      return cuda_ok(cudaStreamSynchronize(s_out), err, "gemm_host sync") ? TT_OK : TT_E_CUDA;
+      const bool ok = cuda_ok(cudaStreamSynchronize(s_out), err, "gemm_host sync");
+      if (trace) {
+        cudaDeviceSynchronize();
+        for (auto& [what, e] : tev) {
+          float ms = 0.f;
+          cudaEventElapsedTime(&ms, tev[0].second, e);
+          std::fprintf(stderr, "[host pipeline] %-10s %8.1f us\n", what.c_str(), ms * 1e3);
+          cudaEventDestroy(e);
+        }
+      }
+      return ok ? TT_OK : TT_E_CUDA;
     }
   }
   // Row-chunked pipeline (NN layout): B, then A chunk i, on the copy-in stream; GEMM of chunk i

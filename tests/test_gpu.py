@@ -515,6 +515,7 @@ def _tail_rows(sp_lib, cfg, M):
     (3, ((16, 2, 1, 128), (32, 128), (16, 1, 1, 256))),    # bf16 4096^3 driver-bench config (r1 BENCH)
     (3, ((8, 2, 2, 128), (64, 64), (16, 1, 1, 256))),      # bf16 4096^3 round-2 baseline best
     (2, ((8, 2, 2, 128), (128, 32), (16, 1, 1, 256))),     # tf32 4096^3 best (profiles/r7_workloads)
+    (2, ((16, 2, 1, 128), (64, 64), (16, 1, 1, 256))),     # tf32 4096^3 round-2 best (wave+remainder split)
 ])
 def test_umma_best_configs_4096_default_policy(fam, cfg):
     # the reported 4096^3 launches under the DEFAULT tail-split policy, rows crossing the split tiles
@@ -527,8 +528,8 @@ def test_umma_best_configs_4096_default_policy(fam, cfg):
     R = og.gemm_f64_rows(A, B, rows)
     assert og.normwise_error(C[rows], R) <= 5e-3, (cfg, info.split_tiles)
     assert not np.isnan(C).any()
-    if fam == tt.FAM_BF16_UMMA and cfg[1] == (32, 128):
-        assert info.split_tiles > 0                       # the driver's headline launch splits its tail
+    if cfg[0] == (16, 2, 1, 128) and cfg[2] == (16, 1, 1, 256):
+        assert info.split_tiles == 256 % 74 + 74          # the headline launches split the last wave + tail
 
 
 def test_simt_best_config_4096_sampled_rows():
