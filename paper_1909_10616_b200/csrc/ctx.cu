@@ -542,12 +542,15 @@ tt_status Ctx::gemm_host(const Space& sp, const State& s, const void* Ah, const 
       const bool ok = cuda_ok(cudaStreamSynchronize(s_out), err, "gemm_host sync");
       if (trace) {
         cudaDeviceSynchronize();
-        for (auto& [what, e] : tev) {
+        for (size_t q = 0; q < tev.size(); ++q) {
           float ms = 0.f;
-          cudaEventElapsedTime(&ms, tev[0].second, e);
-          std::fprintf(stderr, "[host pipeline] %-10s %8.1f us\n", what.c_str(), ms * 1e3);
-          cudaEventDestroy(e);
+          const cudaError_t te = cudaEventElapsedTime(&ms, tev[0].second, tev[q].second);
+          std::fprintf(stderr, "[host pipeline] %-10s %8.1f us%s\n", tev[q].first.c_str(), ms * 1e3,
+                       te == cudaSuccess ? "" : " (no timing)");
         }
+        std::fflush(stderr);
+        for (auto& te : tev) cudaEventDestroy(te.second);
+        cudaGetLastError();
       }
       return ok ? TT_OK : TT_E_CUDA;
     }
