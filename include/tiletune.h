@@ -243,6 +243,16 @@ tt_status tt_neighbors(const tt_space* sp, const tt_config* cfg, tt_config* out,
 /* Launch binding of a feasible config (grid, block, smem, stages, descriptors). */
 tt_status tt_binding(const tt_space* sp, const tt_config* cfg, tt_launch_info* info);
 
+/* Introspection of the tcgen05 families' persistent schedule (DESIGN.md §6 tail / wave+remainder
+ * split): the work items cluster `worker` walks, in order, as the kernel computes them (the same
+ * code, evaluated on the host under the current TT_TAIL_SPLIT policy; without a GPU the cluster
+ * count is SMs / cluster size).  Each item is 5 int32: tile, first k-block, end k-block, order
+ * (pieces of the tile below this one), split flag.  Writes min(cap, n) items to `items` (may be
+ * null with cap 0), the item count to *n_items, the number of clusters to *workers and k0 (k-blocks
+ * per tile) to *k0.  TT_E_UNSUPPORTED for the SIMT family. */
+tt_status tt_umma_schedule(const tt_space* sp, const tt_config* cfg, int32_t worker, int32_t* items, int32_t cap,
+                           int32_t* n_items, int32_t* workers, int32_t* k0);
+
 /* ---------------------------------------------------------------- device: generator, GEMM */
 
 /* K4: fill `count` elements with the counter-based U[-1,1) recipe of DESIGN.md §5 for matrix

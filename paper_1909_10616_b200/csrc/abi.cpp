@@ -305,6 +305,28 @@ tt_status tt_binding(const tt_space* sp, const tt_config* cfg, tt_launch_info* i
   return r == TT_OK ? TT_OK : fail(r, err);
 }
 
+tt_status tt_umma_schedule(const tt_space* sp, const tt_config* cfg, int32_t worker, int32_t* items, int32_t cap,
+                           int32_t* n_items, int32_t* workers, int32_t* k0) {
+  CHECK_SPACE(sp);
+  if (!cfg || !n_items || !workers || !k0 || cap < 0 || (cap > 0 && !items)) return fail(TT_E_INVAL, "null argument");
+  if (sp->family != TT_FAM_TF32_UMMA && sp->family != TT_FAM_BF16_UMMA)
+    return fail(TT_E_UNSUPPORTED, "schedule introspection is for the tcgen05 families");
+  Space s(*sp, false);
+  State st = from_cfg(*cfg);
+  if (!s.j_prod(st)) return fail(TT_E_ILLEGITIMATE, "J_prod false");
+  if (!s.j_hw(st)) return fail(TT_E_INFEASIBLE, "J_hw false");
+  std::vector<std::vector<int32_t>> per;
+  std::string err;
+  tt_status r = tt::umma_schedule(s, st, &per, k0, &err);
+  if (r != TT_OK) return fail(r, err);
+  *workers = (int32_t)per.size();
+  if (worker < 0 || worker >= (int32_t)per.size()) return fail(TT_E_INVAL, "worker out of range");
+  const auto& v = per[(size_t)worker];
+  *n_items = (int32_t)(v.size() / 5);
+  for (int32_t i = 0; i < std::min(cap, *n_items) * 5; ++i) items[i] = v[(size_t)i];
+  return TT_OK;
+}
+
 tt_status tt_fill_uniform(void* dst, int32_t dtype, uint64_t seed, uint64_t idx0, uint64_t count, void* stream) {
   if (!dst && count) return fail(TT_E_INVAL, "null dst");
   if (dtype != 0 && dtype != 1) return fail(TT_E_INVAL, "dtype must be 0 (fp32) or 1 (bf16)");

@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "space.hpp"
 
@@ -42,6 +43,9 @@ tt_status simt_prepare(const Space& sp, const State& s, std::string* err);
 tt_status simt_preload(std::string* err);
 tt_status umma_preload(int family, std::string* err);
 tt_status umma_bind(const Space& sp, const State& s, tt_launch_info* info, std::string* err);
+// every cluster's work items (tile, kb0, kb1, order, split) x n of a tcgen05 launch, in walk order
+tt_status umma_schedule(const Space& sp, const State& s, std::vector<std::vector<int32_t>>* per_worker,
+                        int32_t* k0, std::string* err);
 tt_status umma_prepare(const Space& sp, const State& s, const void* A, const void* B, float* C, std::string* err);
 tt_status umma_launch(const Space& sp, const State& s, const void* A, const void* B, float* C,
                       cudaStream_t stream, std::string* err);

@@ -335,10 +335,10 @@ struct Sched {
   // (plan_of), and 64-bit divisions (a called subroutine each) cost ~1 us of prologue.
   int w, P, dp, nseg, seg;
   uint32_t b, e;
-  __device__ __forceinline__ static uint32_t sk_begin(const UmmaArgs& p, int v) {
+  __host__ __device__ __forceinline__ static uint32_t sk_begin(const UmmaArgs& p, int v) {
     return (uint32_t)v * ((uint32_t)p.sk_tiles * (uint32_t)p.k0) / (uint32_t)p.sk_workers;
   }
-  __device__ __forceinline__ Sched(const UmmaArgs& p, int w_, int P_) : w(w_), P(P_), dp(w_), nseg(0), seg(0), b(0), e(0) {
+  __host__ __device__ __forceinline__ Sched(const UmmaArgs& p, int w_, int P_) : w(w_), P(P_), dp(w_), nseg(0), seg(0), b(0), e(0) {
     if (w < p.sk_workers) {
       b = sk_begin(p, w);
       e = sk_begin(p, w + 1);
@@ -346,7 +346,7 @@ struct Sched {
     }
   }
   // tail pieces first, last tile of the range first; then the data-parallel tiles
-  __device__ __forceinline__ bool next(const UmmaArgs& p, Item* it) {
+  __host__ __device__ __forceinline__ bool next(const UmmaArgs& p, Item* it) {
     if (seg < nseg) {
       const uint32_t k0 = (uint32_t)p.k0;
       const uint32_t t_rel = (e - 1) / k0 - (uint32_t)seg;
@@ -1080,6 +1080,28 @@ tt_status umma_bind(const Space& sp, const State& s, tt_launch_info* info, std::
   info->idesc = pl.a.idesc;
   info->split_tiles = pl.a.sk_tiles;
   info->split_workers = pl.a.sk_workers;
+  (void)err;
+  return TT_OK;
+}
+
+// Work items of every cluster of a config's tcgen05 launch, in the order the kernel's roles walk
+// them: the same Sched code the kernel runs, evaluated on the host (tt_umma_schedule; CPU tests
+// check coverage and the lower-index-only wait order of the split pieces).
+tt_status umma_schedule(const Space& sp, const State& s, std::vector<std::vector<int32_t>>* per_worker,
+                        int32_t* k0, std::string* err) {
+  Plan pl;
+  plan_of(sp, s, &pl);
+  const int P = pl.grid / pl.csize;
+  per_worker->assign(P, {});
+  for (int w = 0; w < P; ++w) {
+    Sched sch(pl.a, w, P);
+    Item it;
+    while (sch.next(pl.a, &it)) {
+      auto& v = (*per_worker)[w];
+      v.insert(v.end(), {it.tile, it.kb0, it.kb1, it.order, it.split ? 1 : 0});
+    }
+  }
+  *k0 = pl.a.k0;
   (void)err;
   return TT_OK;
 }

@@ -92,6 +92,8 @@ EXPORTS = {
     "tt_step": (i32, [C.POINTER(Space), C.POINTER(Config), i32, i32, i32, C.POINTER(Config), C.POINTER(i32)]),
     "tt_neighbors": (i32, [C.POINTER(Space), C.POINTER(Config), C.POINTER(Config), i32, C.POINTER(i32)]),
     "tt_binding": (i32, [C.POINTER(Space), C.POINTER(Config), C.POINTER(LaunchInfo)]),
+    "tt_umma_schedule": (i32, [C.POINTER(Space), C.POINTER(Config), i32, C.POINTER(i32), i32, C.POINTER(i32),
+                               C.POINTER(i32), C.POINTER(i32)]),
     "tt_fill_uniform": (i32, [vp, i32, u64, u64, u64, vp]),
     "tt_gemm": (i32, [i64, i64, i64, i32, vp, vp, vp, C.POINTER(Config), vp]),
     "tt_gemm_ex": (i32, [i64, i64, i64, i32, i32, vp, vp, vp, C.POINTER(Config), vp]),
@@ -230,6 +232,23 @@ def neighbors(sp: Space, s: State) -> List[State]:
     _check(lib.tt_neighbors(C.byref(sp), C.byref(to_config(s)), buf, 64, C.byref(n)), "neighbors")
     d = _depths(sp)
     return [from_config(buf[i], d) for i in range(n.value)]
+
+
+def umma_schedule(sp: Space, s: State):
+    """tt_umma_schedule for every cluster: (k0, [[(tile, kb0, kb1, order, split), ...] per cluster])."""
+    n, workers, k0 = i32(), i32(), i32()
+    cfg = to_config(s)
+    _check(lib.tt_umma_schedule(C.byref(sp), C.byref(cfg), 0, None, 0, C.byref(n), C.byref(workers), C.byref(k0)),
+           "umma_schedule")
+    out = []
+    for w in range(workers.value):
+        _check(lib.tt_umma_schedule(C.byref(sp), C.byref(cfg), w, None, 0, C.byref(n), C.byref(workers),
+                                    C.byref(k0)), "umma_schedule")
+        buf = (i32 * max(5 * n.value, 1))()
+        _check(lib.tt_umma_schedule(C.byref(sp), C.byref(cfg), w, buf, n.value, C.byref(n), C.byref(workers),
+                                    C.byref(k0)), "umma_schedule")
+        out.append([tuple(buf[5 * i:5 * i + 5]) for i in range(n.value)])
+    return k0.value, out
 
 
 def binding(sp: Space, s: State) -> LaunchInfo:

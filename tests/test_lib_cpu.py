@@ -393,3 +393,43 @@ def test_scoring_opts_reading_z12():
     assert fixed.cut_s == 0.5                          # an explicit cut is kept
     bf = tt.make_space(4096, 4096, 4096, family=tt.FAM_BF16_UMMA)
     assert tt.roofline_seconds(bf) < tt.roofline_seconds(tt.make_space(4096, 4096, 4096, family=tt.FAM_F32_SIMT)) / 16
+
+
+@pytest.mark.parametrize("mode", ["1", "2", "3", "4"])
+@pytest.mark.parametrize("fam,dims,cfg", [
+    (3, (4096, 4096, 4096), ((16, 2, 1, 128), (32, 128), (16, 1, 1, 256))),   # bench config: 256 pair tiles
+    (3, (2048, 2048, 512), ((16, 1, 1, 128), (8, 64), (16, 1, 1, 128))),      # 256 single-CTA tiles
+    (3, (2048, 2048, 512), ((8, 2, 1, 128), (8, 64), (8, 1, 1, 256))),        # 64 pair tiles < 74 pairs
+    (3, (2048, 2048, 512), ((16, 1, 1, 128), (8, 64), (16, 2, 1, 64))),       # n1 = 2 clusters
+    (2, (4096, 4096, 4096), ((16, 2, 1, 128), (64, 64), (16, 1, 1, 256))),    # tf32 best (round 2)
+    (3, (1024, 8192, 8192), ((2, 2, 2, 128), (128, 64), (32, 1, 2, 128))),   # 8-GPU shard
+])
+def test_umma_schedule_covers_and_waits_only_on_lower_clusters(mode, fam, dims, cfg, monkeypatch):
+    # the persistent tcgen05 schedule (the kernel's own Sched code, evaluated on the
+    # host) gives every (tile, k-block) to exactly one cluster; a split tile's pieces combine in
+    # ascending k (order = pieces below); and every piece that waits (order > 0) waits only on
+    # pieces that are the FIRST item of a LOWER-index cluster -- the deadlock-freedom argument
+    # (no co-residency assumption), for every split policy.
+    monkeypatch.setenv("TT_TAIL_SPLIT", mode)
+    M, N, K = dims
+    sp = tt.make_space(M, N, K, family=fam)
+    assert tt.is_legitimate(sp, cfg) == (True, True)
+    k0, per = tt.umma_schedule(sp, cfg)
+    tiles = cfg[0][0] * cfg[2][0]
+    owner = {}
+    pieces = {}
+    for w, items in enumerate(per):
+        for q, (tile, kb0, kb1, order, split) in enumerate(items):
+            assert 0 <= tile < tiles and 0 <= kb0 < kb1 <= k0
+            assert bool(split) == (not (kb0 == 0 and kb1 == k0))
+            for kb in range(kb0, kb1):
+                assert (tile, kb) not in owner            # covered at most once
+                owner[(tile, kb)] = (w, q)
+            pieces.setdefault(tile, []).append((kb0, kb1, order, w, q))
+    assert len(owner) == tiles * k0                       # ... and at least once
+    for tile, ps in pieces.items():
+        ps.sort()
+        for rank, (kb0, kb1, order, w, q) in enumerate(ps):
+            assert order == rank                          # ascending-k combine order
+            for (b0, b1, o2, v, q2) in ps[:rank]:
+                assert v < w and q2 == 0                  # waits only on lower clusters' first items
