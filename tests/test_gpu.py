@@ -5,6 +5,7 @@ sequential fmaf oracle and <= 1e-4 vs double; TF32 / BF16 <= 5e-3 vs double on t
 the device consumed (bf16-rounded for BF16, reading Z16; fp32 for TF32, reading Z17).
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -22,6 +23,7 @@ from oracle.space import Spec  # noqa: E402
 from paper_1909_10616_b200 import tiletune as tt  # noqa: E402
 
 DEV = torch.device("cuda:0")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def host_inputs(M, N, K, bf16=False, row0=0):
@@ -689,3 +691,53 @@ def test_partial_grid_probe_estimates_slow_simt():
     fast = ((8, 2, 8, 8), (64, 16), (8, 4, 4, 8))          # 64 CTAs: never probed partially
     assert ctx.measure(sp, fast, tt.measure_opts(cut_s=1e-3)).slow_cut == 0
     ctx.close()
+
+
+def _trace_lib():
+    """The trace build of the library, built on first use."""
+    lib = os.path.join(ROOT, "build", "variants", "trace", "libtiletune.so")
+    if not os.path.exists(lib):
+        from paper_1909_10616_b200 import build as b
+        lib = b.build_variant("trace", ["TT_UMMA_TRACE_BUILD"])
+    return lib
+
+
+@pytest.mark.parametrize("mode,M,N,K,cfg", [
+    ("1", 4096, 4096, 4096, ((16, 2, 1, 128), (32, 128), (16, 1, 1, 256))),   # bench launch: wave + remainder
+    ("2", 2048, 2048, 512, ((16, 1, 1, 128), (8, 64), (16, 1, 1, 128))),      # round-1 tail split, forced
+    ("4", 2048, 2048, 512, ((16, 1, 1, 128), (8, 64), (16, 2, 1, 64))),       # wave + remainder, n1 = 2
+])
+def test_device_schedule_matches_host(mode, M, N, K, cfg, tmp_path):
+    # The items every cluster's epilogue actually processed (trace build, TT_UMMA_TRACE) are, in
+    # order, the ones tt_umma_schedule computes on the host -- so the CPU schedule-invariant test
+    # (coverage, ascending-k combine, lower-index-only waits) is a statement about the device.
+    import subprocess
+    import sys as _sys
+    out = tmp_path / "trace.bin"
+    env = dict(os.environ, TT_LIB_PATH=_trace_lib(), TT_UMMA_TRACE=str(out), TT_TAIL_SPLIT=mode)
+    code = ("import torch, json, sys; sys.path.insert(0, %r); from paper_1909_10616_b200 import tiletune as tt; "
+            "M, N, K = %d, %d, %d; cfg = %r; "
+            "A = torch.randn(M, K, device='cuda').to(torch.bfloat16); B = torch.randn(K, N, device='cuda').to(torch.bfloat16); "
+            "C = torch.empty(M, N, device='cuda'); tt.gemm(A, B, C, tt.FAM_BF16_UMMA, cfg); torch.cuda.synchronize()"
+            % (ROOT, M, N, K, cfg))
+    subprocess.run([_sys.executable, "-c", code], env=env, check=True, timeout=600)
+    raw = np.fromfile(out, dtype=np.uint64)
+    ncl, nit = int(raw[0]), int(raw[1])
+    tr = raw[4:4 + ncl * nit * 8].reshape(ncl, nit, 8).astype(np.int64)
+    os.environ["TT_TAIL_SPLIT"] = mode
+    try:
+        k0, per = tt.umma_schedule(tt.make_space(M, N, K, family=tt.FAM_BF16_UMMA), cfg)
+    finally:
+        del os.environ["TT_TAIL_SPLIT"]
+    # the trace is sized grid / cta_group; with n1 = 2 only the first grid / cluster-size rows
+    # (one per cluster, cluster_id = blockIdx / cluster size) are written
+    assert len(per) <= ncl and not tr[len(per):, :, 2].any()
+    for c in range(len(per)):
+        dev = []
+        for i in range(nit):
+            if tr[c, i, 2] == 0:                       # slot 2 = MMA start time: 0 = no such item
+                break
+            w = int(tr[c, i, 1])
+            dev.append((int(tr[c, i, 0]), w & 0xFFFF, (w >> 16) & 0xFFFF, w >> 32))
+        host = [(t, a, b, o) for (t, a, b, o, _) in per[c]][:nit]
+        assert dev == host, (c, dev, host)
