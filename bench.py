@@ -237,11 +237,11 @@ def tune(ctx, sp, Mr, N, K, fam, layout, budget, args, world, coll, local):
     raw, feasible = tt.count_configs(sp, feasible=True)
     sopts = tt.search_opts(family=fam, seed=args.seed, width=args.width, layout=layout,
                            measure={"l2_flush": 1 if args.tune_l2_flush else 0})
-    ms_fn, observe, cut_fn = tdist.device_measure_set(ctx, sp, sopts, device=local)
+    ms_fn, observe, cut_fn, mp_fn = tdist.device_measure_set(ctx, sp, sopts, device=local)
     store = tdist.default_store() if (world > 1 and args.assign in ("dynamic", "auto")) else None
     ev = tdist.TrackingEvaluator(observe=observe, measure_set=ms_fn, device=coll if world > 1 else None,
                                  store=store, assign="lpt" if (args.assign in ("dynamic", "auto") and store is None) else args.assign,
-                                 space=sp, cut_s=cut_fn)
+                                 space=sp, cut_s=cut_fn, measure_phase=mp_fn if args.two_phase else None)
     ctx.prepare(sp)                      # one-time setup (operands, flush buffer, kernels loaded) off the clock
     if world > 1:
         dist.barrier()
@@ -256,49 +256,74 @@ def tune(ctx, sp, Mr, N, K, fam, layout, budget, args, world, coll, local):
            "speculative_measured": ev.spec_measured, "speculative_used": ev.spec_used,
            "scoring": ("L2 flushed before every timed launch" if args.tune_l2_flush else "warm L2, CUDA-graph replay")
            + "; slow cut min(max(20 cost_min, 1 ms), 50 t_roof), racing at 1.1 cost_min after 2 repeats (reading Z12)",
-           "assignment": ev.assign}
+           "assignment": ev.assign + (" + two-phase rounds" if args.two_phase else ""),
+           "round_modes": ev.round_modes}
     if getattr(args, "dump_tuning", None) and (not dist.is_initialized() or dist.get_rank() == 0):
         with open(args.dump_tuning + f".{sp.family}_{Mr}.jsonl", "w") as f:
-            for k, (ts, ws) in enumerate(zip(ev.round_times, ev.round_weights)):
-                f.write(json.dumps({"round": k, "secs": ts, "weights": ws}) + "\n")
+            for k, (ts, ws, ph) in enumerate(zip(ev.round_times, ev.round_weights, ev.round_phase1)):
+                f.write(json.dumps({"round": k, "secs": ts, "weights": ws, "mode": ev.round_modes[k],
+                                    "phase1": [list(x) for x in ph]}) + "\n")
             for r in res.trace:
                 f.write(json.dumps({"state": r["state"], "cost": r["cost"], "t": r["t_wall_s"]}) + "\n")
     if world == 1:
         # Projection of the sharded search from this run's per-candidate
-        # measurement times: each round's candidates assigned by rule, the slowest rank gates the
-        # round, + 50 us per round for the exchange; the host search work is replicated on every
+        # measurement times: the evaluator's own planning code (weights, assignment, speculation,
+        # two-phase rounds) replayed for G ranks on the recorded costs (dist.simulate_sharded);
+        # the slowest rank gates each phase, + 50 us per exchange, + the measured cost of one
+        # dynamic claim; the host search work (everything but measuring) is replicated on every
         # rank.  Not a multi-GPU measurement (the driver's N = 2/4/8 runs measure tuning_wall_s).
-        meas = sum(sum(t) for t in ev.round_times)
-        host = max(0.0, tune_wall - meas)
-        proj = {}
-        nb = {}
-
-        def neighbors(x):
-            if x not in nb:
-                nb[x] = tt.neighbors(sp, x)
-            return nb[x]
-
-        kw = dict(per_round_s=50e-6, states=ev.round_states, neighbors=neighbors)
-        for G in (2, 4, 8):
-            ws = host + tdist.projected_sharded_wall(ev.round_times, G, **kw)
-            wl = host + tdist.projected_sharded_wall(ev.round_times, G, weights=ev.round_weights, **kw)
-            wd = host + tdist.projected_sharded_wall(ev.round_times, G, dynamic=True, per_claim_s=200e-6,
-                                                     weights=ev.round_weights, **kw)
-            wa = host + tdist.projected_sharded_wall(ev.round_times, G, auto=True, per_claim_s=200e-6,
-                                                     weights=ev.round_weights, **kw)
-            proj[str(G)] = {"auto_wall_s": wa, "auto_speedup": tune_wall / wa if wa > 0 else None,
-                            "dynamic_wall_s": wd, "dynamic_speedup": tune_wall / wd if wd > 0 else None,
-                            "lpt_wall_s": wl, "lpt_speedup": tune_wall / wl if wl > 0 else None,
-                            "static_wall_s": ws, "static_speedup": tune_wall / ws if ws > 0 else None}
-        rec["projected_sharded_search"] = {"rounds": ev.rounds, "round_sizes": [len(t) for t in ev.round_times],
-                                           "measure_s": meas, "host_s": host, "by_gpus": proj,
-                                           "model": "round by round: slowest rank's measurement time + 50 us exchange; "
-                                                    "dynamic = claims in LPT order (200 us each); auto (the N > 1 "
-                                                    "default) = dynamic in rounds whose median predicted candidate "
-                                                    "time is >= 2 ms, else LPT; round 0 speculates g(s0) on the idle "
-                                                    "ranks; host search work replicated",
-                                           "kind": "projection from 1-GPU per-candidate times"}
+        claim = claim_seconds(ctx, sp, ev.round_states[-1][:1])
+        rec["projected_sharded_search"] = project_sharded(
+            ev, tune_wall, sp, lambda b: tt.scoring_opts(sp, sopts, b, local).cut_s, claim)
     return res.best, rec
+
+
+def project_sharded(ev, tune_wall, sp, cut_of, claim):
+    """Projection of the one-GPU search recorded by ``ev`` (a ShardedEvaluator) onto 2, 4 and 8
+    ranks for each assignment variant: host work other than planning (tune_wall - measuring -
+    planning) is replicated, the planning and the measurement come from dist.simulate_sharded."""
+    from paper_1909_10616_b200 import dist as tdist
+    meas = sum(sum(t) for t in ev.round_times)
+    host = max(0.0, tune_wall - meas - ev.plan_s)       # replicated host work other than planning
+    rcosts = [[ev.known[s] for s in st] for st in ev.round_states]
+    proj = {}
+    variants = (("two_phase", dict(assign="auto", two_phase=True)), ("lpt", dict(assign="lpt")),
+                ("dynamic", dict(assign="dynamic")), ("static", dict(assign="static", speculate=False)))
+    for G in (2, 4, 8):
+        e = {}
+        for name, kw in variants:
+            r = tdist.simulate_sharded(ev.round_states, rcosts, ev.round_times, G, space=sp, cut_of=cut_of,
+                                       round_phase1=ev.round_phase1, per_round_s=50e-6, per_claim_s=claim, **kw)
+            w = host + r["plan_host_s"] + r["wall_s"]
+            e[name + "_wall_s"] = w
+            e[name + "_speedup"] = tune_wall / w if w > 0 else None
+            if name == "two_phase":
+                e["two_phase_rounds"] = r["modes"].count("two-phase")
+        proj[str(G)] = e
+    return {"rounds": ev.rounds, "round_sizes": [len(t) for t in ev.round_times], "measure_s": meas,
+            "host_s": host, "plan_s_1gpu": ev.plan_s, "claim_s": claim, "by_gpus": proj,
+            "model": "the evaluator's planning code replayed for G ranks on this run's costs and per-candidate "
+                     "seconds (dist.simulate_sharded): per phase the slowest rank + 50 us exchange; two_phase "
+                     "(the N > 1 default) = probes, exchange, then the rest of each measurement balanced with the "
+                     "probes known; dynamic claims cost claim_s (measured here: a TCPStore add + one measure "
+                     "call's marshalling); round 0 speculates g(s0) on the idle ranks; host search work other "
+                     "than planning replicated (host_s), planning re-timed per G",
+            "kind": "projection from 1-GPU per-candidate times"}
+
+
+def claim_seconds(ctx, sp, states, n=200):
+    """Cost of one dynamic claim on this host: a TCPStore add round trip (loopback, as on one
+    node) plus one measure call's argument marshalling with nothing to measure."""
+    import datetime
+
+    import torch.distributed as dist
+    st = dist.TCPStore("127.0.0.1", 0, 1, True, timeout=datetime.timedelta(seconds=10), wait_for_workers=False)
+    st.add("warm", 1)
+    t0 = time.perf_counter()
+    for _ in range(n):
+        st.add("claim", 1)
+        ctx.measure_set(sp, states, [False] * len(states))
+    return (time.perf_counter() - t0) / n
 
 
 def time_gemm(tt, A, B, C, fam, best, layout, steps, warmup, flush, world, sampler=None):
@@ -427,6 +452,9 @@ def main():
                     help="how a round's candidates are spread over the ranks (paper_1909_10616_b200/dist.py)")
     ap.add_argument("--layout", choices=["nn", "tn"], default="nn",
                     help="tn: A stored as W[K][M] (the paper's perceptron Y = W^T X, P:372)")
+    ap.add_argument("--one-phase", dest="two_phase", action="store_false",
+                    help="sharded rounds measure each candidate whole on one rank (default: two-phase rounds, "
+                         "probes first, then the rest balanced with the probes known)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--ref-rows", type=int, default=16)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define TT_VERSION 5
+#define TT_VERSION 6
 #define TT_MAXD 4  /* maximum loop depth per axis carried in tt_config */
 
 typedef enum {
@@ -343,6 +343,24 @@ tt_status tt_scoring_opts(const tt_space* sp, int32_t device, const tt_search_op
  * set to 0.  Stops at the first failing candidate (its status is returned). */
 tt_status tt_measure_set(tt_ctx* ctx, const tt_space* sp, const tt_config* cfgs, int32_t n, const uint8_t* mine,
                          const tt_measure_opts* mo, double* costs, double* secs);
+
+/* Two-phase form of tt_measure_set for the sharded evaluator (reading Z12).  Splits
+ * one measurement at its cold probe so that a round can be balanced over ranks with the probe
+ * known: the probe alone decides whether a candidate is cut (one launch) and predicts whether
+ * racing stops it after race_repeats, i.e. how long the rest takes.
+ *   phase 1: for j with mine == NULL or mine[j] != 0, run the (partial-grid and) cold probe of
+ *            cfgs[j].  If that decides the score (slow cut, tt_sample.slow_cut != 0) then
+ *            values[j] = the score and final_[j] = 1; else values[j] = probe seconds, final_[j] = 0.
+ *   phase 2: run the rest of tt_measure (warm-ups, warm probe, R repeats with racing) for
+ *            cfgs[j] as if its cold probe had returned probes[j] (> 0, from phase 1, possibly on
+ *            another device of the same model); values[j] = cost_s, final_[j] = 1.
+ * Phase 1 then phase 2 on one device performs exactly the launches of one tt_measure and gives
+ * the same statistic.  Other entries are set to 0; secs[j] (nullable) = host wall seconds of that
+ * phase.  values, final_ (and probes for phase 2) hold n entries, caller-owned.  Errors as
+ * tt_measure_set; TT_E_INVAL for another phase, or a phase-2 probe <= 0. */
+tt_status tt_measure_phase(tt_ctx* ctx, const tt_space* sp, const tt_config* cfgs, int32_t n, const uint8_t* mine,
+                           const tt_measure_opts* mo, int32_t phase, const double* probes, double* values,
+                           uint8_t* final_, double* secs);
 
 /* The statistic tt_measure reports ("the arithmetic mean for 10 repeated trials"; reading
  * Z10): from R >= 1 per-repeat mean launch times per_repeat[0..R) (seconds, host array), sets

@@ -551,6 +551,46 @@ tt_status tt_measure_set(tt_ctx* ctx, const tt_space* sp, const tt_config* cfgs,
   return TT_OK;
 }
 
+tt_status tt_measure_phase(tt_ctx* ctx, const tt_space* sp, const tt_config* cfgs, int32_t n, const uint8_t* mine,
+                           const tt_measure_opts* mo, int32_t phase, const double* probes, double* values,
+                           uint8_t* final_, double* secs) {
+  CHECK_SPACE(sp);
+  if (!ctx || (n > 0 && (!cfgs || !values || !final_)) || n < 0) return fail(TT_E_INVAL, "null argument");
+  if (phase != 1 && phase != 2) return fail(TT_E_INVAL, "phase must be 1 or 2");
+  if (phase == 2 && n > 0 && !probes) return fail(TT_E_INVAL, "phase 2 needs the phase-1 probes");
+  if (sp->family == TT_FAM_NONE) return fail(TT_E_UNSUPPORTED, "family NONE has no kernel");
+  tt_measure_opts m;
+  if (mo) m = *mo;
+  else tt_measure_opts_default(&m);
+  Space s(*sp, false);
+  Ctx* c = static_cast<Ctx*>(ctx);
+  for (int32_t j = 0; j < n; ++j) {
+    values[j] = 0.0;
+    final_[j] = 0;
+    if (secs) secs[j] = 0.0;
+  }
+  for (int32_t j = 0; j < n; ++j) {
+    if (mine && !mine[j]) continue;
+    State st = from_cfg(cfgs[j]);
+    if (!s.j_prod(st)) return fail(TT_E_ILLEGITIMATE, "J_prod false");
+    if (!s.j_hw(st)) return fail(TT_E_INFEASIBLE, "J_hw false");
+    if (phase == 2 && !(probes[j] > 0)) return fail(TT_E_INVAL, "phase 2 needs a positive probe");
+    const auto t0 = std::chrono::steady_clock::now();
+    tt_sample smp;
+    std::string err;
+    tt_status r = c->measure(s, st, m, &smp, &err, phase, phase == 2 ? probes[j] : 0.0);
+    if (r != TT_OK) return fail(r, err);
+    if (phase == 1 && smp.repeats == 0) {
+      values[j] = smp.probe_s;
+    } else {
+      values[j] = smp.cost_s;
+      final_[j] = 1;
+    }
+    if (secs) secs[j] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+  return TT_OK;
+}
+
 tt_status tt_gbfs_search(tt_ctx* ctx, int64_t M, int64_t N, int64_t K, uint64_t budget_evals,
                          const tt_search_opts* opts, tt_result* out, tt_trace_row* trace, uint64_t trace_cap) {
   return run_search(gbfs_search, ctx, M, N, K, budget_evals, opts, out, trace, trace_cap);

@@ -265,7 +265,7 @@ tt_status Ctx::flush_l2(std::string* err) {
 }
 
 tt_status Ctx::measure(const Space& sp, const State& s, const tt_measure_opts& mo, tt_sample* out,
-                       std::string* err) {
+                       std::string* err, int phase, double probe_in) {
   NvtxRange nv("tt_measure");
   DeviceGuard g(device);
   if (!cuda_ok(g.status, err, "cudaSetDevice")) return TT_E_CUDA;
@@ -294,7 +294,7 @@ tt_status Ctx::measure(const Space& sp, const State& s, const tt_measure_opts& m
   // rows; when that extrapolates past the cut, the candidate is scored by the estimate (slow_cut = 2)
   // and never runs in full.  CTAs are independent tiles, so a row prefix of the grid is a valid
   // partial launch, and the waves of such configs take equal time.
-  if (mo.cut_s > 0 && sp.family == TT_FAM_F32_SIMT) {
+  if (phase != 2 && mo.cut_s > 0 && sp.family == TT_FAM_F32_SIMT) {
     int64_t ctas = 0, slots = 0;
     if ((st = simt_probe_shape(sp, s, &ctas, &slots, err)) != TT_OK) return st;
     const int64_t n0 = s.f[2][0];                       // CTAs per grid row (grid.x)
@@ -323,8 +323,8 @@ tt_status Ctx::measure(const Space& sp, const State& s, const tt_measure_opts& m
       }
     }
   }
-  double probe = 0;
-  if ((st = timed_once(&probe)) != TT_OK) return st;
+  double probe = probe_in;
+  if (phase != 2 && (st = timed_once(&probe)) != TT_OK) return st;
   out->probe_s = probe;
   out->device = device;
   if (mo.cut_s > 0 && probe > mo.cut_s) {  // Z12
@@ -334,6 +334,7 @@ tt_status Ctx::measure(const Space& sp, const State& s, const tt_measure_opts& m
     out->slow_cut = 1;
     return TT_OK;
   }
+  if (phase == 1) return TT_OK;              // probe only: repeats = 0 marks "not final"
   // warm-up launches only matter when the repeats run warm: under the L2 flush every timed launch
   // starts cold (reading Z11), and the cold probe has already run the config once
   const int warm = mo.l2_flush ? 0 : (mo.warmup >= 0 ? mo.warmup : 2);

@@ -50,7 +50,10 @@ struct Ctx : tt_ctx {
   tt_status operands(const Space& sp, Operands** out, std::string* err);
   tt_status flush_l2(std::string* err);
   tt_status prepare(const Space& sp, std::string* err);
-  tt_status measure(const Space& sp, const State& s, const tt_measure_opts& mo, tt_sample* out, std::string* err);
+  // phase 0: the whole measurement; 1: the cold probe only (out->repeats = 0 unless the probe
+  // alone decides the score); 2: everything after the probe, given probe_in (tt_measure_phase)
+  tt_status measure(const Space& sp, const State& s, const tt_measure_opts& mo, tt_sample* out, std::string* err,
+                    int phase = 0, double probe_in = 0.0);
   tt_status gemm_host(const Space& sp, const State& s, const void* Ah, const void* Bh, float* Ch, std::string* err);
 };
 

@@ -24,10 +24,14 @@ import torch.distributed as dist
 
 from . import tiletune as tt
 
-# measurement-time model of one candidate for the LPT assignment: a candidate scored by its
-# probe costs one launch, a full one ~11 (cold probe, 10 repeats), plus host overhead
+# measurement-time model of one candidate for the LPT assignment (reading Z12's scoring rules): a
+# candidate above the slow cut is scored by its probe (1 launch); below it, the probe and R = 10
+# repeats (11 launches) unless racing stops it after 2 repeats (3) -- predicted when its predicted
+# cost exceeds 1.1 x the incumbent.  Every launch costs the GEMM plus an overhead (L2 flush, events,
+# host) that the evaluator calibrates from the exchanged (cost, seconds) of the measured candidates.
 _FULL_LAUNCHES = 11
-_PER_CANDIDATE_S = 2e-3
+_RACED_LAUNCHES = 3
+_RACE_RATIO = 1.1
 # one dynamic claim (a TCPStore add round trip); "auto" claims dynamically only in rounds whose
 # median predicted measurement time is >= _AUTO_CLAIMS claims, else it uses the LPT plan
 _CLAIM_S = 200e-6
@@ -38,7 +42,7 @@ def auto_mode(weights: Sequence[float]) -> str:
     """The "auto" rule for one round (identical on every rank: the weights come from the
     replicated known costs): dynamic claiming when the median predicted measurement time is at
     least _AUTO_CLAIMS claim round trips, else the LPT plan (no per-candidate store traffic)."""
-    raw = sorted(w - _PER_CANDIDATE_S for w in weights)
+    raw = sorted(weights)
     med = raw[len(raw) // 2] if raw else 0.0
     return "dynamic" if med >= _AUTO_CLAIMS * _CLAIM_S else "lpt"
 
@@ -81,7 +85,7 @@ class ShardedEvaluator:
     def __init__(self, measure_one: Optional[Callable] = None, group=None, device: Optional[torch.device] = None,
                  store=None, measure_set: Optional[Callable] = None, assign: Optional[str] = None,
                  space: Optional[tt.Space] = None, cut_s: Optional[Callable[[], float]] = None,
-                 speculate: bool = True):
+                 speculate: bool = True, measure_phase: Optional[Callable] = None):
         if measure_set is None:
             if measure_one is None:
                 raise ValueError("need measure_one or measure_set")
@@ -95,6 +99,7 @@ class ShardedEvaluator:
                         secs[j] = time.perf_counter() - t0
                 return costs, secs
         self.measure_set = measure_set
+        self.measure_phase = measure_phase
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -113,12 +118,21 @@ class ShardedEvaluator:
         self.rounds = 0
         self.local_evals = 0
         self.known: dict = {}
+        self._known_code: dict = {}              # packed-exponent key -> cost (see _code)
+        self._move_deltas = None
+        self.plan_s = 0.0                        # host seconds spent planning rounds (replicated work)
+        self._over = 0.0                         # calibrated per-launch overhead (weights)
+        self._over_obs: List[float] = []
         self._nb_cache: dict = {}
         self.speculate = speculate
         self.cache: dict = {}                # speculative costs not yet requested by the search
         self.spec_measured = 0
         self.spec_used = 0
         self.round_states: List[list] = []
+        self.round_spec: List[tuple] = []        # per round: (speculative states, their seconds)
+        # per round, two-phase rounds only (else empty lists): phase-1 seconds, probe values, and
+        # whether the probe alone decided the score
+        self.round_phase1: List[tuple] = []
         # per round: (measurement seconds of every candidate on the rank that measured it -- the
         # values are exchanged with the costs --, predicted weights used by the LPT assignment)
         self.round_times: List[List[float]] = []
@@ -135,9 +149,7 @@ class ShardedEvaluator:
     def _moves(s):
         """Every state one action away from s (Eq. 6: s_x[i] <- 2 s_x[i], s_x[j] <- s_x[j] / 2, s_x[j]
         even), legitimate or not.  Only measured -- hence legitimate -- states are ever looked up in
-        the known costs, so min over these equals min over the legitimate neighbours g(s); pure
-        Python, because this runs on every rank for every candidate (a ctypes tt_neighbors call per
-        candidate cost ~50 us, a third of a bf16 search's host time)."""
+        the known costs, so min over these equals min over the legitimate neighbours g(s)."""
         for a, f in enumerate(s):
             for i in range(len(f)):
                 for j in range(len(f)):
@@ -147,24 +159,113 @@ class ShardedEvaluator:
                         g[j] //= 2
                         yield s[:a] + (tuple(g),) + s[a + 1:]
 
-    def _predicted_cost(self, s) -> float:
-        best = math.inf
-        if self.space is not None:
-            for t in self._moves(s):
-                c = self.known.get(t)
-                if c is not None and c < best:
-                    best = c
-        if not math.isfinite(best):
-            best = min(self.known.values()) if self.known else 1.0
-        return best
+    _codes: dict = {}                          # state -> packed code (None: not all powers of two)
 
-    def weights(self, states) -> List[float]:
+    @classmethod
+    def _code(cls, s):
+        """Packed log2 exponents (5 bits per factor, outer to inner, m then k then n) when every
+        factor is a power of two (the paper's square 2^j problems), else None.  An action of Eq. 6
+        is then one integer add: +1 on exponent i, -1 on exponent j of the same axis."""
+        code = cls._codes.get(s, -1)
+        if code != -1:
+            return code
+        code, sh = 0, 0
+        for f in s:
+            for v in f:
+                if v & (v - 1):
+                    cls._codes[s] = None
+                    return None
+                code |= (v.bit_length() - 1) << sh
+                sh += 5
+        if len(cls._codes) > 1 << 20:
+            cls._codes.clear()
+        cls._codes[s] = code
+        return code
+
+    def _deltas(self, s):
+        d = self._move_deltas
+        if d is None:
+            d, base = [], 0
+            for f in s:
+                L = len(f)
+                for i in range(L):
+                    for j in range(L):
+                        if i != j:
+                            d.append(((1 << 5 * (base + i)) - (1 << 5 * (base + j)), 5 * (base + j)))
+                base += L
+            self._move_deltas = d
+        return d
+
+    def _predicted_cost(self, s) -> float:
+        """Geometric mean of the known costs of the states one action away from s (measured
+        states are legitimate, so these are its measured neighbours in g(s)); the minimum known
+        cost if none is known.  On the measured bf16 4096^3 costs it classifies racing correctly
+        for 83 % of the candidates, the neighbours' minimum for 74 % (tools/spec_study.py).  Pure
+        Python over packed exponents: this runs on every rank for every candidate (a ctypes
+        tt_neighbors call per candidate costs ~50 us)."""
+        acc, n = 0.0, 0
+        if self.space is not None:
+            c = self._code(s)
+            if c is not None:
+                get = self._known_code.get
+                log = math.log
+                for d, sh in self._deltas(s):
+                    if (c >> sh) & 31:
+                        v = get(c + d)
+                        if v is not None:
+                            acc += log(v)
+                            n += 1
+            else:
+                for t in self._moves(s):
+                    v = self.known.get(t)
+                    if v is not None:
+                        acc += math.log(v)
+                        n += 1
+        if n:
+            return math.exp(acc / n)
+        return min(self.known.values()) if self.known else 1.0
+
+    def set_known(self, known: dict):
+        """Replace the known costs (tests; the search fills them round by round)."""
+        self.known = {}
+        self._known_code = {}
+        for s, c in known.items():
+            self._remember(s, c)
+
+    def _remember(self, s, c):
+        self.known[s] = c
+        k = self._code(s)
+        if k is not None:
+            self._known_code[k] = c
+
+    @staticmethod
+    def launches(c: float, best: float, cut: float) -> int:
+        """Launches the scoring rules (reading Z12) spend on a candidate of cost c at incumbent
+        ``best`` and slow cut ``cut`` (0 = none)."""
+        if cut > 0 and c > cut:
+            return 1
+        if math.isfinite(best) and c > _RACE_RATIO * best:
+            return _RACED_LAUNCHES
+        return _FULL_LAUNCHES
+
+    def weights(self, states, preds: Optional[Sequence[float]] = None) -> List[float]:
+        """Predicted measurement seconds of each state: launches(predicted cost) x (predicted cost +
+        calibrated per-launch overhead).  Identical on every rank (exchanged costs only)."""
         cut = self.cut_s() if self.cut_s is not None else 0.0
-        w = []
-        for s in states:
-            c = self._predicted_cost(s)
-            w.append((c if (cut > 0 and c > cut) else _FULL_LAUNCHES * c) + _PER_CANDIDATE_S)
-        return w
+        best = min(self.known.values()) if self.known else math.inf
+        o = self._over
+        if preds is None:
+            preds = [self._predicted_cost(s) for s in states]
+        return [self.launches(c, best, cut) * (c + o) for c in preds]
+
+    def _calibrate(self, costs, secs, best, cut):
+        """Per-launch overhead = median over measured candidates of secs / launches - cost."""
+        for c, t in zip(costs, secs):
+            if c > 0 and t > 0:
+                self._over_obs.append(max(0.0, t / self.launches(c, best, cut) - c))
+        if self._over_obs:
+            v = sorted(self._over_obs)
+            self._over = v[len(v) // 2]
 
     @staticmethod
     def lpt_owners(weights: Sequence[float], world: int) -> List[int]:
@@ -179,35 +280,161 @@ class ShardedEvaluator:
         return owner
 
     # ------------------------------------------------------------------ one round
-    def _speculative(self, states) -> List:
-        """States the idle ranks measure while a round that has fewer candidates than ranks runs:
-        the round-0 neighbourhood g(s0) (Eq. 9 under reading Z4), in action order.  Round 1 of
-        G-BFS draws its candidates from exactly that set (Alg. 1 line 6), so it then costs no
-        measurement; the traversal is unchanged (costs are looked up, never re-drawn)."""
-        if not self.speculate or self.rounds != 0 or self.world <= len(states) or self.space is None:
-            return []
-        seen = set(states) | set(self.known) | set(self.cache)
-        out = []
-        for s in states:
-            for t in self._neighbors(s):
-                if t not in seen:
-                    seen.add(t)
-                    out.append(t)
-        return out
+    def _speculative(self, sub, wts, owner):
+        """States measured speculatively in this round, and their ranks.
+
+        Round 0 (s0 alone, fewer candidates than ranks): the idle ranks measure g(s0) (Eq. 9
+        under reading Z4), from which round 1 of G-BFS draws all of its candidates (Alg. 1 line
+        6) -- every state, spread over the idle ranks.
+        (Speculating later rounds -- the unmeasured neighbours of the states the next G-BFS round
+        is expected to pop, filling each rank's idle time -- was simulated on the measured bf16
+        4096^3 costs, tools/spec_study.py: with W = 16 the ranks' idle time rarely fits a whole
+        candidate and it bought nothing, so it is not built.)
+        The traversal is unchanged either way: a speculative cost is only looked up when the
+        search requests that state (never re-drawn)."""
+        if not self.speculate or self.space is None or self.world <= 1:
+            return [], []
+        if self.rounds == 0:
+            if self.world <= len(sub):
+                return [], []
+            seen = set(sub) | set(self.known) | set(self.cache)
+            out = []
+            for s in sub:
+                for t in self._neighbors(s):
+                    if t not in seen:
+                        seen.add(t)
+                        out.append(t)
+            if owner is None:
+                return out, None
+            busy = set(owner)
+            idle = [r for r in range(self.world) if r not in busy] or list(range(self.world))
+            return out, [idle[i % len(idle)] for i in range(len(out))]
+        return [], []
+
+    def plan(self, states):
+        """The round's plan, identical on every rank (it depends only on the exchanged costs):
+        (hit, todo, wts, mode, owner, spec, spec_owner).  ``owner`` is None for dynamic claims;
+        ``spec_owner`` is None when speculative states are claimed dynamically."""
+        hit = [s in self.cache for s in states]         # measured speculatively in an earlier round
+        todo = [j for j in range(len(states)) if not hit[j]]
+        sub = [states[j] for j in todo]
+        m = len(sub)
+        preds = [self._predicted_cost(s) for s in sub] if self.assign in ("lpt", "dynamic", "auto") else None
+        wts = self.weights(sub, preds) if preds is not None else [1.0] * m
+        mode = auto_mode(wts) if self.assign == "auto" else self.assign
+        if self.two_phase(m, mode):
+            # phase 1 = the cold probes, balanced by the predicted probe time (one launch each)
+            mode = "two-phase"
+            o = self._over
+            owner = self.lpt_owners([c + o for c in preds], self.world)
+            return hit, todo, sub, wts, mode, owner, [], []
+        if mode == "dynamic" and self.world > 1:
+            owner = None
+        elif mode == "lpt":
+            owner = self.lpt_owners(wts, self.world)
+        else:
+            owner = [j % self.world for j in range(m)]
+        spec, spec_owner = self._speculative(sub, wts, owner)
+        return hit, todo, sub, wts, mode, owner, spec, spec_owner
+
+    def two_phase(self, m: int, mode: str) -> bool:
+        """A round runs in two phases (probes, exchange, then the rest of each measurement balanced
+        with the probes known; tt_measure_phase) when the evaluator has a phase measurer, the round
+        has more candidates than ranks, and its candidates are not claimed dynamically."""
+        return self.measure_phase is not None and m > self.world and mode != "dynamic" and self.assign != "static"
+
+    def phase2_plan(self, probes, final, cut):
+        """Owners of the phase-2 work (None for candidates the probe finished) and its predicted
+        seconds: (launches(probe) - 1) x (probe + overhead) -- the racing prediction now uses the
+        measured probe instead of the neighbours' costs."""
+        best = min(self.known.values()) if self.known else math.inf
+        o = self._over
+        idx = [j for j in range(len(probes)) if not final[j]]
+        w2 = [(self.launches(probes[j], best, cut) - 1) * (probes[j] + o) for j in idx]
+        own = self.lpt_owners(w2, self.world)
+        owner2 = [None] * len(probes)
+        for q, j in enumerate(idx):
+            owner2[j] = own[q]
+        return owner2, w2
+
+    def _exchange(self, vals):
+        """all_reduce(MAX) of a host float vector whose entries only the owning rank filled."""
+        buf = torch.tensor(vals, dtype=torch.float64, device=self.device)
+        dist.all_reduce(buf, op=dist.ReduceOp.MAX, group=self.group)
+        return buf.cpu().tolist()
+
+    def _two_phase(self, sub, owner, cut, vals):
+        """Measure a round in two phases; fills vals[:m] (costs) and vals[m:2m] (seconds, both
+        phases) like the one-phase path and returns per candidate (phase-1 seconds, probe or
+        final value, final?).  Phase 1: each rank probes its LPT share, one exchange.  Phase 2:
+        the unfinished candidates' remaining launches, LPT over the probe-based predictions, a
+        second exchange.  A candidate's repeats may run on another rank than its probe (same GPU
+        model; under the L2 flush every timed launch starts cold, and the probe only decides the
+        cut and the prediction)."""
+        m = len(sub)
+        mine = [o == self.rank for o in owner]
+        v1 = [0.0] * (3 * m)                   # value, final flag, seconds
+        if any(mine):
+            val, fin, sec = self.measure_phase(sub, mine, 1, None)
+            for j in range(m):
+                if mine[j]:
+                    v1[j], v1[m + j], v1[2 * m + j] = val[j], 1.0 if fin[j] else 0.0, sec[j]
+        if self.world > 1:
+            v1 = self._exchange(v1)
+        probes = v1[:m]
+        final = [v1[m + j] > 0.5 for j in range(m)]
+        t0 = time.perf_counter()
+        owner2, _ = self.phase2_plan(probes, final, cut)
+        self.plan_s += time.perf_counter() - t0
+        mine2 = [o == self.rank for o in owner2]
+        v2 = [0.0] * (2 * m)
+        for j in range(m):
+            if final[j] and owner[j] == self.rank:
+                v2[j] = probes[j]
+        if any(mine2):
+            val, _, sec = self.measure_phase(sub, mine2, 2, probes)
+            for j in range(m):
+                if mine2[j]:
+                    v2[j], v2[m + j] = val[j], sec[j]
+                    self.local_evals += 1
+        for j in range(m):
+            if final[j] and owner[j] == self.rank:
+                self.local_evals += 1
+        if self.world > 1:
+            v2 = self._exchange(v2)
+        for j in range(m):
+            vals[j] = v2[j]
+            vals[m + j] = v1[2 * m + j] + v2[m + j]
+        return [(v1[2 * m + j], probes[j], final[j]) for j in range(m)]
+
+    def absorb(self, states, costs, spec, spec_costs, secs=None, cut=0.0):
+        """Record a finished round: requested costs become known, their measurement seconds
+        calibrate the weight model, speculative costs wait in the cache until requested."""
+        if secs is not None:
+            self._calibrate(costs, secs, min(self.known.values()) if self.known else math.inf, cut)
+        for i, t in enumerate(spec):
+            if spec_costs[i] > 0:
+                self.cache[t] = spec_costs[i]
+                self.spec_measured += 1
+        for s, c in zip(states, costs):
+            self._remember(s, c)
+        self.round_states.append(list(states))
+        self.rounds += 1
 
     def __call__(self, states: Sequence) -> List[float]:
         n = len(states)
-        hit = [s in self.cache for s in states]         # measured speculatively in an earlier round
-        todo = [j for j in range(n) if not hit[j]]
-        sub = [states[j] for j in todo]
+        t0 = time.perf_counter()
+        cut = self.cut_s() if self.cut_s is not None else 0.0
+        hit, todo, sub, wts, mode, owner, spec, spec_owner = self.plan(states)
+        self.plan_s += time.perf_counter() - t0
         m = len(sub)
-        wts = self.weights(sub) if self.assign in ("lpt", "dynamic", "auto") else [1.0] * m
-        mode = auto_mode(wts) if self.assign == "auto" else self.assign
         self.round_modes.append(mode)
-        spec = self._speculative(sub)
         S = len(spec)
         vals = [0.0] * (2 * m + 2 * S)          # costs, seconds (this round), then speculative costs, seconds
-        if mode == "dynamic" and self.world > 1:
+        p1 = None
+        if mode == "two-phase":
+            p1 = self._two_phase(sub, owner, cut, vals)
+        elif owner is None:
             # claim in longest-predicted-first order (LPT order) from a shared counter
             order = sorted(range(m), key=lambda j: (-wts[j], j))
             key = f"{self.ns}_round{self.rounds}"
@@ -226,12 +453,7 @@ class ShardedEvaluator:
                         break
                     c, t = self.measure_set(spec, [i == q for i in range(S)])
                     vals[2 * m + q], vals[2 * m + S + q] = c[q], t[q]
-            spec_owner = []
         else:
-            if mode == "lpt":
-                owner = self.lpt_owners(wts, self.world)
-            else:
-                owner = [j % self.world for j in range(m)]
             mine = [o == self.rank for o in owner]
             if any(mine):
                 c, t = self.measure_set(sub, mine)
@@ -239,21 +461,16 @@ class ShardedEvaluator:
                     if mine[j]:
                         vals[j], vals[m + j] = c[j], t[j]
                         self.local_evals += 1
-            busy = set(owner)
-            idle = [r for r in range(self.world) if r not in busy] or list(range(self.world))
-            spec_owner = [idle[i % len(idle)] for i in range(S)]
-        if S and spec_owner:
             smine = [o == self.rank for o in spec_owner]
             if any(smine):
                 c, t = self.measure_set(spec, smine)
                 for i in range(S):
                     if smine[i]:
                         vals[2 * m + i], vals[2 * m + S + i] = c[i], t[i]
+        if self.world > 1 and p1 is None:
+            vals = self._exchange(vals)
         if self.world > 1:
-            buf = torch.tensor(vals, dtype=torch.float64, device=self.device)
-            dist.all_reduce(buf, op=dist.ReduceOp.MAX, group=self.group)
-            vals = buf.cpu().tolist()
-            if mode == "dynamic" and self.rank == 0:
+            if owner is None and self.rank == 0:
                 for k in (f"{self.ns}_round{self.rounds}", f"{self.ns}_round{self.rounds}_spec"):
                     try:                                 # every rank has left its claim loops
                         self.store.delete_key(k)
@@ -269,17 +486,18 @@ class ShardedEvaluator:
                 self.spec_used += 1
         if not all(c > 0 for c in costs):
             raise RuntimeError(f"sharded round {self.rounds}: a candidate came back unmeasured ({costs})")
-        for i in range(S):
-            if vals[2 * m + i] > 0:
-                self.cache[spec[i]] = vals[2 * m + i]
-                self.spec_measured += 1
         self.round_times.append(secs)
         self.round_weights.append([w for w in wts] if m == n else
                                   [wts[todo.index(j)] if not hit[j] else 0.0 for j in range(n)])
-        self.round_states.append(list(states))
-        self.rounds += 1
-        for s, c in zip(states, costs):
-            self.known[s] = c
+        self.round_spec.append((list(spec), vals[2 * m + S:2 * m + 2 * S]))
+        if p1 is not None:
+            ph = [(0.0, 0.0, False)] * n
+            for q, j in enumerate(todo):
+                ph[j] = p1[q]
+            self.round_phase1.append(tuple(zip(*ph)))
+        else:
+            self.round_phase1.append(([], [], []))
+        self.absorb(states, costs, spec, vals[2 * m:2 * m + S], secs=secs, cut=cut)
         return costs
 
 
@@ -296,8 +514,9 @@ def device_measure_set(ctx: tt.Context, sp: tt.Space, opts: tt.SearchOpts, devic
     """measure_set for ShardedEvaluator on the device: one tt_measure_set call per round with the
     search's scoring options (tt_scoring_opts: slow-candidate cut and racing, reading Z12) at the
     incumbent -- identical on every rank, because it is the minimum of the exchanged costs.
-    Returns (measure_set, observe, cut_s) where observe(costs) updates the incumbent and cut_s()
-    is the current cut (for the LPT weights)."""
+    Returns (measure_set, observe, cut_s, measure_phase) where observe(costs) updates the
+    incumbent, cut_s() is the current cut (for the weights) and measure_phase(states, mine, phase,
+    probes) is the two-phase form (tt_measure_phase)."""
     state = {"best": math.inf}
 
     def mo():
@@ -306,86 +525,114 @@ def device_measure_set(ctx: tt.Context, sp: tt.Space, opts: tt.SearchOpts, devic
     def measure_set(states, mine):
         return ctx.measure_set(sp, states, mine, mo())
 
+    def measure_phase(states, mine, phase, probes):
+        return ctx.measure_phase(sp, states, mine, phase, probes, mo())
+
     def observe(costs):
         for c in costs:
             state["best"] = min(state["best"], c)
 
-    return measure_set, observe, lambda: mo().cut_s
+    return measure_set, observe, lambda: mo().cut_s, measure_phase
 
 
-def _busy(times: Sequence[float], world: int, mode: str, weights: Optional[Sequence[float]], per_claim_s: float):
-    """Per-rank busy time of one round's candidates under an assignment rule."""
-    busy = [0.0] * world
-    if mode == "dynamic":                                  # list scheduling, LPT order if weighted
-        order = sorted(range(len(times)), key=lambda j: (-weights[j], j)) if weights is not None else range(len(times))
-        for j in order:
-            r = min(range(world), key=lambda i: busy[i])
-            busy[r] += times[j] + per_claim_s
-    else:
-        owner = ShardedEvaluator.lpt_owners(weights, world) if mode == "lpt" else [j % world for j in range(len(times))]
-        for j, t in enumerate(times):
-            busy[owner[j]] += t
-    return busy
+def simulate_sharded(round_states: Sequence[Sequence], round_costs: Sequence[Sequence[float]],
+                     round_times: Sequence[Sequence[float]], world: int, *, space: Optional[tt.Space],
+                     assign: str = "lpt", speculate: bool = True, two_phase: bool = False,
+                     round_phase1: Optional[Sequence[tuple]] = None,
+                     cut_of: Optional[Callable[[float], float]] = None, spec_time: Optional[Callable] = None,
+                     per_round_s: float = 50e-6, per_claim_s: float = 200e-6) -> dict:
+    """Projection of a recorded search (rounds of requested states, their costs and the seconds
+    each took to measure on one GPU) onto ``world`` ranks by running the evaluator's own planning
+    code (``ShardedEvaluator.plan`` / ``phase2_plan`` / ``absorb``: weights, assignment,
+    speculation, two-phase rounds) with the recorded costs.  Per round: the slowest rank's busy
+    time (its candidates' recorded seconds, plus ``per_claim_s`` per dynamic claim) +
+    ``per_round_s`` per exchange (two in a two-phase round).  Two-phase rounds split a candidate's
+    seconds at its probe: the recorded phase-1 seconds and probe value when the one-GPU run was
+    two-phase too (``round_phase1``, ShardedEvaluator.round_phase1), else one launch's share
+    (seconds / launches(cost)) with probe = cost.  A speculative state costs its recorded seconds
+    if the search measured it at some point, else ``spec_time(state)`` (default: the median
+    recorded candidate).  ``cut_of(incumbent)`` gives the slow cut the weights assume
+    (tt.scoring_opts), none if omitted.  Speculation and assignment cannot change the traversal,
+    so the recorded rounds are exactly what the sharded run requests.  Returns {"wall_s",
+    "plan_host_s" (the planning code's own host time), "spec_measured", "spec_used", "modes"}.
+    A projection from one-GPU times, not a multi-GPU measurement."""
+    ev = ShardedEvaluator(measure_set=lambda st, mi: ([0.0] * len(st), [0.0] * len(st)), space=space,
+                          speculate=speculate, assign=assign if assign in ("lpt", "static") else "lpt",
+                          measure_phase=(lambda *a: None) if two_phase else None)
+    ev.world, ev.rank = world, 0
+    if cut_of is not None:
+        ev.cut_s = lambda: cut_of(min(ev.known.values())) if ev.known else 0.0
+    if assign in ("dynamic", "auto") and world > 1:
+        ev.assign = assign
+    rec = {}
+    for rs, rt in zip(round_states, round_times):
+        for s, t in zip(rs, rt):
+            rec.setdefault(s, t)
+    allt = sorted(t for rt in round_times for t in rt)
+    med = allt[len(allt) // 2] if allt else 0.0
 
+    def t_of(s):
+        if s in rec:
+            return rec[s]
+        return spec_time(s) if spec_time is not None else med
 
-def projected_sharded_wall(round_times: Sequence[Sequence[float]], world: int, per_round_s: float = 0.0,
-                           dynamic: bool = False, per_claim_s: float = 0.0,
-                           weights: Optional[Sequence[Sequence[float]]] = None,
-                           states: Optional[Sequence[Sequence]] = None, neighbors: Optional[Callable] = None,
-                           auto: bool = False) -> float:
-    """Measurement wall time of the same traversal sharded over ``world`` ranks, from
-    per-candidate times recorded on one rank: sum over rounds of the slowest rank's busy time,
-    plus ``per_round_s`` (the exchange) per round.  Static: candidate j on rank j mod world.
-    ``weights`` given: the evaluator's LPT assignment from those predicted weights (with
-    ``dynamic``: claims in that order).  Dynamic: each candidate goes to the rank that becomes
-    free first, each claim costing ``per_claim_s``.  ``states`` + ``neighbors`` given: the
-    speculative round 0 (ShardedEvaluator.speculate) -- the idle ranks measure g(s0) while s0 runs,
-    each such state costing what it cost when the search measured it (else the dearest of them),
-    and later rounds do not re-measure those states.  ``auto`` (needs ``weights``): each round
-    dynamic or LPT by the evaluator's auto rule (``auto_mode``).  A projection from measured
-    times, not a multi-GPU measurement."""
-    mode = "dynamic" if dynamic else ("lpt" if weights is not None else "static")
-    if auto:
-        mode = "auto"
-    spec_t = {}
-    if states is not None and neighbors is not None and world > 1 and round_times and len(round_times[0]) < world:
-        seen = set(states[0])
-        order = []
-        for s0 in states[0]:
-            for t in neighbors(s0):
-                if t not in seen:
-                    seen.add(t)
-                    order.append(t)
-        when = {}
-        for k in range(1, len(states)):
-            for s, t in zip(states[k], round_times[k]):
-                when.setdefault(s, t)
-        known = [when[t] for t in order if t in when]
-        fallback = max(known) if known else max(round_times[0])
-        spec_t = {t: when.get(t, fallback) for t in order}
-    total = 0.0
-    for k, times in enumerate(round_times):
-        w = weights[k] if weights is not None else None
-        if spec_t and k > 0:
-            keep = [j for j, s in enumerate(states[k]) if s not in spec_t]
-            times = [times[j] for j in keep]
-            w = [w[j] for j in keep] if w is not None else None
-            for s in states[k]:                            # a speculative state is served once
-                spec_t.pop(s, None)
-        rmode = (auto_mode(weights[k]) if weights is not None else "static") if mode == "auto" else mode
-        busy = _busy(times, world, rmode, w, per_claim_s)
-        if spec_t and k == 0:
-            st = list(spec_t.values())
-            if rmode == "dynamic":
-                for t in st:
-                    r = min(range(world), key=lambda i: busy[i])
-                    busy[r] += t + per_claim_s
+    def lpt_busy(owner, times):
+        busy = [0.0] * world
+        for j, r in enumerate(owner):
+            if r is not None:
+                busy[r] += times[j]
+        return max(busy)
+
+    wall = host = 0.0
+    modes = []
+    for k, states in enumerate(round_states):
+        t0 = time.perf_counter()
+        cut = ev.cut_s() if ev.cut_s is not None else 0.0
+        best = min(ev.known.values()) if ev.known else math.inf
+        hit, todo, sub, wts, mode, owner, spec, spec_owner = ev.plan(list(states))
+        host += time.perf_counter() - t0
+        modes.append(mode)
+        times = [round_times[k][j] for j in todo]
+        if mode == "two-phase":
+            ph = round_phase1[k] if round_phase1 is not None and k < len(round_phase1) else None
+            if ph is not None and len(ph[0]):
+                t1 = [ph[0][j] for j in todo]
+                probes = [ph[1][j] for j in todo]
+                final = [bool(ph[2][j]) for j in todo]
             else:
-                idle = [r for r in range(world) if busy[r] == 0.0] or list(range(world))
-                for i, t in enumerate(st):
-                    busy[idle[i % len(idle)]] += t
-        total += (max(busy) if busy else 0.0) + (per_round_s if world > 1 else 0.0)
-    return total
+                cs = [round_costs[k][j] for j in todo]
+                nl = [ev.launches(c, best, cut) for c in cs]
+                t1 = [t / n for t, n in zip(times, nl)]
+                probes = cs
+                final = [n == 1 for n in nl]
+            t0 = time.perf_counter()
+            owner2, _ = ev.phase2_plan(probes, final, cut)
+            host += time.perf_counter() - t0
+            t2 = [t - a for t, a in zip(times, t1)]
+            wall += lpt_busy(owner, t1) + lpt_busy(owner2, t2) + (2 * per_round_s if world > 1 else 0.0)
+        else:
+            busy = [0.0] * world
+            if owner is None:                               # dynamic claims in LPT order
+                for j in sorted(range(len(sub)), key=lambda j: (-wts[j], j)):
+                    r = min(range(world), key=lambda i: busy[i])
+                    busy[r] += times[j] + per_claim_s
+                for s in spec:
+                    r = min(range(world), key=lambda i: busy[i])
+                    busy[r] += t_of(s) + per_claim_s
+            else:
+                for j, r in enumerate(owner):
+                    busy[r] += times[j]
+                for s, r in zip(spec, spec_owner):
+                    busy[r] += t_of(s)
+            wall += max(busy) + (per_round_s if world > 1 else 0.0)
+        for j, s in enumerate(states):
+            if hit[j]:
+                ev.cache.pop(s)
+                ev.spec_used += 1
+        ev.absorb(list(states), list(round_costs[k]), spec, [1.0] * len(spec),
+                  secs=[0.0 if hit[j] else round_times[k][j] for j in range(len(states))], cut=cut)
+    return {"wall_s": wall, "plan_host_s": host, "spec_measured": ev.spec_measured, "spec_used": ev.spec_used,
+            "modes": modes}
 
 
 class TrackingEvaluator(ShardedEvaluator):

@@ -111,6 +111,9 @@ EXPORTS = {
     "tt_scoring_opts": (i32, [C.POINTER(Space), i32, C.POINTER(SearchOpts), dbl, C.POINTER(MeasureOpts)]),
     "tt_measure_set": (i32, [vp, C.POINTER(Space), C.POINTER(Config), i32, C.POINTER(C.c_uint8),
                              C.POINTER(MeasureOpts), C.POINTER(dbl), C.POINTER(dbl)]),
+    "tt_measure_phase": (i32, [vp, C.POINTER(Space), C.POINTER(Config), i32, C.POINTER(C.c_uint8),
+                               C.POINTER(MeasureOpts), i32, C.POINTER(dbl), C.POINTER(dbl), C.POINTER(C.c_uint8),
+                               C.POINTER(dbl)]),
     "tt_measure": (i32, [vp, C.POINTER(Space), C.POINTER(Config), C.POINTER(MeasureOpts), C.POINTER(Sample)]),
     "tt_gbfs_search": (i32, [vp, i64, i64, i64, u64, C.POINTER(SearchOpts), C.POINTER(Result),
                              C.POINTER(TraceRow), u64]),
@@ -433,6 +436,21 @@ class Context:
         _check(lib.tt_measure_set(self.h, C.byref(sp), cfgs, n, mk, C.byref(opts) if opts else None, costs, secs),
                "measure_set")
         return [costs[j] for j in range(n)], [secs[j] for j in range(n)]
+
+    def measure_phase(self, sp: Space, states: Sequence[State], mine: Optional[Sequence[bool]], phase: int,
+                      probes: Optional[Sequence[float]] = None, opts: Optional[MeasureOpts] = None):
+        """tt_measure_phase: (values, final, secs) of the states with mine[j] true (phase 1: the
+        cold probe, or the final score when the probe decides it; phase 2: the rest given probes)."""
+        n = len(states)
+        cfgs = (Config * max(n, 1))(*[to_config(s) for s in states])
+        mk = (C.c_uint8 * max(n, 1))(*[1 if m else 0 for m in mine]) if mine is not None else None
+        pr = (dbl * max(n, 1))(*[float(p) for p in probes]) if probes is not None else None
+        vals = (dbl * max(n, 1))()
+        fin = (C.c_uint8 * max(n, 1))()
+        secs = (dbl * max(n, 1))()
+        _check(lib.tt_measure_phase(self.h, C.byref(sp), cfgs, n, mk, C.byref(opts) if opts else None, phase, pr,
+                                    vals, fin, secs), "measure_phase")
+        return [vals[j] for j in range(n)], [bool(fin[j]) for j in range(n)], [secs[j] for j in range(n)]
 
     def gemm_host(self, A_host, B_host, C_host, family: int, s: State, layout: int = LAYOUT_NN):
         M, N, K = _check_gemm_operands(A_host, B_host, C_host, family, layout, on_device=False)

@@ -34,3 +34,46 @@ def test_warmup_floor():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--warmup", "1"], capture_output=True,
                        text=True, timeout=120)
     assert r.returncode != 0
+
+
+def test_sharded_projection_of_a_recorded_search():
+    # bench.project_sharded on a one-rank search with fake two-phase measurements (no GPU): the
+    # projection replays the evaluator's plans for G = 2, 4, 8 and reports every variant
+    import hashlib
+    import time
+
+    import bench
+    from paper_1909_10616_b200 import dist as tdist
+    from paper_1909_10616_b200 import tiletune as tt
+
+    M = 4096
+    sp = tt.make_space(M, M, M, family=tt.FAM_BF16_UMMA)
+
+    def cost(s):
+        h = hashlib.sha256(repr(s).encode()).digest()
+        return 9e-5 + int.from_bytes(h[:4], "little") / 2 ** 32 * 3e-4
+
+    def measure_set(states, mine):
+        return [cost(s) if m else 0.0 for s, m in zip(states, mine)], \
+               [11 * (cost(s) + 7e-5) if m else 0.0 for s, m in zip(states, mine)]
+
+    def measure_phase(states, mine, phase, probes):
+        vals = [cost(s) if m else 0.0 for s, m in zip(states, mine)]
+        secs = [(cost(s) + 7e-5) * (1 if phase == 1 else 10) if m else 0.0 for s, m in zip(states, mine)]
+        return vals, [phase == 2] * len(states), secs
+
+    ev = tdist.ShardedEvaluator(measure_set=measure_set, measure_phase=measure_phase, space=sp)
+    t0 = time.perf_counter()
+    res = tt.gbfs_search(M, M, M, 128, tt.search_opts(family=tt.FAM_BF16_UMMA, seed=0, width=16), batch=ev)
+    wall = time.perf_counter() - t0 + sum(map(sum, ev.round_times))
+    assert res.evals == 128 and "two-phase" in ev.round_modes
+    assert all(len(p[0]) == len(st) for p, st, md in zip(ev.round_phase1, ev.round_states, ev.round_modes)
+               if md == "two-phase")
+    pr = bench.project_sharded(ev, wall, sp, lambda b: 1e-3, 30e-6)
+    assert pr["round_sizes"] == [len(r) for r in ev.round_states] and pr["rounds"] == ev.rounds
+    for G in ("2", "4", "8"):
+        e = pr["by_gpus"][G]
+        for v in ("two_phase", "lpt", "dynamic", "static"):
+            assert 1.0 < e[v + "_speedup"] <= int(G) + 1e-9
+        assert e["two_phase_rounds"] >= 1
+    assert pr["by_gpus"]["8"]["two_phase_speedup"] > pr["by_gpus"]["2"]["two_phase_speedup"]

@@ -360,6 +360,27 @@ def test_gbfs_device_search_replay_parity():
     assert res.frac_raw == 120 / 484000
 
 
+def test_gbfs_two_phase_evaluator_replay_parity():
+    # the bench's tuning path: G-BFS (W = 16) with the sharded evaluator, device two-phase rounds
+    # (probes, then the rest, tt_measure_phase) on one rank; the traversal replays exactly through
+    # the oracle with the recorded costs, and every round with more than one candidate ran in two
+    # phases
+    from paper_1909_10616_b200 import dist as tdist
+    ctx = tt.Context(0)
+    sp = tt.make_space(2048, 2048, 2048, family=3)
+    sopts = tt.search_opts(family=3, seed=1, width=16, measure={"l2_flush": 1})
+    ms, observe, cut, mp = tdist.device_measure_set(ctx, sp, sopts)
+    ev = tdist.TrackingEvaluator(observe=observe, measure_set=ms, measure_phase=mp, space=sp, cut_s=cut)
+    res = tt.gbfs_search(2048, 2048, 2048, 48, sopts, batch=ev)
+    ctx.close()
+    assert res.evals == 48
+    assert [md == "two-phase" for md in ev.round_modes] == [len(r) > 1 for r in ev.round_states]
+    table = {r["state"]: r["cost"] for r in res.trace}
+    o = ogbfs.gbfs(Spec(2048, 2048, 2048, family=3), lambda states: [table[s] for s in states], budget=48, rho=5,
+                   seed=1, width=16)
+    assert [r.state for r in o.trace] == [r["state"] for r in res.trace]
+
+
 def test_na2c_device_search():
     # live N-A2C (eps = 0.8: policy sampled, networks trained every batch) on the SIMT space of
     # 512^3; replaying its (state -> cost) table through the oracle's Algorithm 2 reproduces the
@@ -655,6 +676,38 @@ def test_measure_racing_and_measure_set():
     costs, secs = ctx.measure_set(sp, [cfg, other, cfg], mine=[True, False, True])
     assert costs[1] == 0.0 and secs[1] == 0.0 and costs[0] > 0 and costs[2] > 0 and secs[0] > 0
     assert abs(costs[0] / won.cost_s - 1) < 0.2
+    ctx.close()
+
+
+def test_measure_phase_splits_one_measurement():
+    # tt_measure_phase (two-phase sharded rounds, §8e): phase 1 = the cold probe (final only when
+    # the slow cut decides the score), phase 2 = the repeats given that probe; together they give
+    # the statistic of one tt_measure, and phase 2 honours racing and the cut with the given probe
+    ctx = tt.Context(0)
+    for fam, M, cfg in ((1, 512, ((4, 2, 8, 8), (64, 8), (4, 4, 4, 8))),
+                        (3, 2048, ((16, 1, 1, 128), (16, 128), (16, 1, 1, 128)))):
+        sp = tt.make_space(M, M, M, family=fam)
+        mo = tt.measure_opts(l2_flush=1)
+        whole = ctx.measure(sp, cfg, mo)
+        v1, f1, s1 = ctx.measure_phase(sp, [cfg, cfg], [True, False], 1, None, mo)
+        assert f1 == [False, False] and v1[1] == 0.0 and s1[1] == 0.0 and v1[0] > 0 and s1[0] > 0
+        assert 0.5 < v1[0] / whole.probe_s < 2.0
+        v2, f2, s2 = ctx.measure_phase(sp, [cfg], [True], 2, [v1[0]], mo)
+        assert f2 == [True] and s2[0] > s1[0]
+        assert abs(v2[0] / whole.cost_s - 1) < 0.2
+        # the cut decides in phase 1 (final), and phase 2 with a probe above the cut returns it
+        cut = tt.measure_opts(l2_flush=1, cut_s=1e-9)
+        v1c, f1c, _ = ctx.measure_phase(sp, [cfg], [True], 1, None, cut)
+        assert f1c == [True] and v1c[0] > 0
+        v2c, _, _ = ctx.measure_phase(sp, [cfg], [True], 2, [0.5], cut)
+        assert v2c == [0.5]
+        # racing in phase 2: stops after race_repeats like tt_measure
+        r2, _, sr = ctx.measure_phase(sp, [cfg], [True], 2, [v1[0]], tt.measure_opts(l2_flush=1, race_s=1e-9))
+        assert r2[0] > 0 and sr[0] < s2[0]
+    with pytest.raises(tt.TileTuneError):
+        ctx.measure_phase(sp, [cfg], [True], 2, [0.0], tt.measure_opts(l2_flush=1))
+    with pytest.raises(tt.TileTuneError):
+        ctx.measure_phase(sp, [cfg], [True], 3, None, tt.measure_opts(l2_flush=1))
     ctx.close()
 
 

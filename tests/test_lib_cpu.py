@@ -27,7 +27,7 @@ def test_abi_exports_every_declared_symbol():
     for name in sorted(declared):
         assert hasattr(tt.lib, name), name
     assert set(tt.EXPORTS) == declared
-    assert tt.lib.tt_version() == 5
+    assert tt.lib.tt_version() == 6
 
 
 @pytest.mark.parametrize("dims,d,fam", [((512, 512, 512), (4, 2, 4), 0), ((1024, 1024, 1024), (4, 2, 4), 0),
