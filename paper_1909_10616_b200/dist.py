@@ -14,11 +14,14 @@ libtiletune call (``tt_measure_set``: the per-rank half of a round runs in C++, 
 """
 from __future__ import annotations
 
+import bisect
+import heapq
 import itertools
 import math
 import time
 from typing import Callable, List, Optional, Sequence, Tuple
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -32,6 +35,11 @@ from . import tiletune as tt
 _FULL_LAUNCHES = 11
 _RACED_LAUNCHES = 3
 _RACE_RATIO = 1.1
+# racing compares the first repeats (not the cold probe) with 1.1 x the incumbent; a probe up to
+# 10 % above that line still often runs the full repeats (measured on the B200: probes sit 1-7 %
+# above the final cost), so phase 2 predicts "raced" only beyond it -- predicting a short
+# candidate long costs an LPT plan little, the converse leaves one rank running at the round's end
+_PROBE_MARGIN = 0.1
 # one dynamic claim (a TCPStore add round trip); "auto" claims dynamically only in rounds whose
 # median predicted measurement time is >= _AUTO_CLAIMS claims, else it uses the LPT plan
 _CLAIM_S = 200e-6
@@ -119,6 +127,8 @@ class ShardedEvaluator:
         self.local_evals = 0
         self.known: dict = {}
         self._known_code: dict = {}              # packed-exponent key -> cost (see _code)
+        self._kc_arrays = None                   # (sorted codes, log costs) for _predicted_costs
+        self._best = math.inf                    # min(known.values())
         self._move_deltas = None
         self.plan_s = 0.0                        # host seconds spent planning rounds (replicated work)
         self._over = 0.0                         # calibrated per-launch overhead (weights)
@@ -225,18 +235,48 @@ class ShardedEvaluator:
             return math.exp(acc / n)
         return min(self.known.values()) if self.known else 1.0
 
+    def _predicted_costs(self, states) -> List[float]:
+        """_predicted_cost of every state at once: on packed codes the neighbour lookups of a whole
+        round are one sorted search over the known codes (numpy); the planning of a round is host
+        work every rank repeats, so it stays off the round's critical path as far as possible."""
+        codes = [self._code(s) for s in states] if self.space is not None else [None]
+        if not states or any(c is None for c in codes) or not self._known_code:
+            return [self._predicted_cost(s) for s in states]
+        if self._kc_arrays is None:
+            ks = sorted(self._known_code)
+            self._kc_arrays = (np.array(ks, dtype=np.int64),
+                               np.array([math.log(self._known_code[k]) for k in ks], dtype=np.float64))
+        K, L = self._kc_arrays
+        dl = self._deltas(states[0])
+        D = np.array([d for d, _ in dl], dtype=np.int64)
+        SH = np.array([sh for _, sh in dl], dtype=np.int64)
+        C = np.array(codes, dtype=np.int64)[:, None]
+        valid = ((C >> SH[None, :]) & 31) != 0
+        nbr = C + D[None, :]
+        idx = np.minimum(np.searchsorted(K, nbr), len(K) - 1)
+        found = valid & (K[idx] == nbr)
+        n = found.sum(axis=1)
+        acc = np.where(found, L[idx], 0.0).sum(axis=1)
+        fallback = min(self.known.values())
+        return [math.exp(a / k) if k else fallback for a, k in zip(acc.tolist(), n.tolist())]
+
     def set_known(self, known: dict):
         """Replace the known costs (tests; the search fills them round by round)."""
         self.known = {}
         self._known_code = {}
+        self._kc_arrays = None
+        self._best = math.inf
         for s, c in known.items():
             self._remember(s, c)
 
     def _remember(self, s, c):
         self.known[s] = c
+        if c < self._best:
+            self._best = c
         k = self._code(s)
         if k is not None:
             self._known_code[k] = c
+            self._kc_arrays = None
 
     @staticmethod
     def launches(c: float, best: float, cut: float) -> int:
@@ -252,19 +292,19 @@ class ShardedEvaluator:
         """Predicted measurement seconds of each state: launches(predicted cost) x (predicted cost +
         calibrated per-launch overhead).  Identical on every rank (exchanged costs only)."""
         cut = self.cut_s() if self.cut_s is not None else 0.0
-        best = min(self.known.values()) if self.known else math.inf
+        best = self._best
         o = self._over
         if preds is None:
-            preds = [self._predicted_cost(s) for s in states]
+            preds = self._predicted_costs(states)
         return [self.launches(c, best, cut) * (c + o) for c in preds]
 
     def _calibrate(self, costs, secs, best, cut):
         """Per-launch overhead = median over measured candidates of secs / launches - cost."""
+        v = self._over_obs                      # kept sorted
         for c, t in zip(costs, secs):
             if c > 0 and t > 0:
-                self._over_obs.append(max(0.0, t / self.launches(c, best, cut) - c))
-        if self._over_obs:
-            v = sorted(self._over_obs)
+                bisect.insort(v, max(0.0, t / self.launches(c, best, cut) - c))
+        if v:
             self._over = v[len(v) // 2]
 
     @staticmethod
@@ -272,11 +312,11 @@ class ShardedEvaluator:
         """Longest-processing-time-first list scheduling: candidates in decreasing weight (ties by
         index) go to the least-loaded rank (ties: lowest rank).  Deterministic."""
         owner = [0] * len(weights)
-        load = [0.0] * world
+        heap = [(0.0, r) for r in range(world)]
         for j in sorted(range(len(weights)), key=lambda j: (-weights[j], j)):
-            r = min(range(world), key=lambda i: (load[i], i))
+            load, r = heapq.heappop(heap)
             owner[j] = r
-            load[r] += weights[j]
+            heapq.heappush(heap, (load + weights[j], r))
         return owner
 
     # ------------------------------------------------------------------ one round
@@ -319,7 +359,7 @@ class ShardedEvaluator:
         todo = [j for j in range(len(states)) if not hit[j]]
         sub = [states[j] for j in todo]
         m = len(sub)
-        preds = [self._predicted_cost(s) for s in sub] if self.assign in ("lpt", "dynamic", "auto") else None
+        preds = self._predicted_costs(sub) if self.assign in ("lpt", "dynamic", "auto") else None
         wts = self.weights(sub, preds) if preds is not None else [1.0] * m
         mode = auto_mode(wts) if self.assign == "auto" else self.assign
         if self.two_phase(m, mode):
@@ -347,10 +387,10 @@ class ShardedEvaluator:
         """Owners of the phase-2 work (None for candidates the probe finished) and its predicted
         seconds: (launches(probe) - 1) x (probe + overhead) -- the racing prediction now uses the
         measured probe instead of the neighbours' costs."""
-        best = min(self.known.values()) if self.known else math.inf
+        best = self._best
         o = self._over
         idx = [j for j in range(len(probes)) if not final[j]]
-        w2 = [(self.launches(probes[j], best, cut) - 1) * (probes[j] + o) for j in idx]
+        w2 = [(self.launches(probes[j] / (1 + _PROBE_MARGIN), best, cut) - 1) * (probes[j] + o) for j in idx]
         own = self.lpt_owners(w2, self.world)
         owner2 = [None] * len(probes)
         for q, j in enumerate(idx):
@@ -411,7 +451,7 @@ class ShardedEvaluator:
         """Record a finished round: requested costs become known, their measurement seconds
         calibrate the weight model, speculative costs wait in the cache until requested."""
         if secs is not None:
-            self._calibrate(costs, secs, min(self.known.values()) if self.known else math.inf, cut)
+            self._calibrate(costs, secs, self._best, cut)
         for i, t in enumerate(spec):
             if spec_costs[i] > 0:
                 self.cache[t] = spec_costs[i]
