@@ -243,6 +243,7 @@ def tune(ctx, sp, Mr, N, K, fam, layout, budget, args, world, coll, local):
                                  store=store, assign="lpt" if (args.assign in ("dynamic", "auto") and store is None) else args.assign,
                                  space=sp, cut_s=cut_fn, measure_phase=mp_fn if args.two_phase else None)
     ctx.prepare(sp)                      # one-time setup (operands, flush buffer, kernels loaded) off the clock
+    ev.warm_up(tt.enumerate_configs(sp, 0, 16))           # host planning code, off the clock too
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()

@@ -243,3 +243,12 @@ def test_auto_mode():
     # auto: dynamic claims only when the median predicted measurement time is >= 10 claims (2 ms)
     assert tdist.auto_mode([1e-3] * 5) == "lpt" and tdist.auto_mode([5e-3] * 5) == "dynamic"
     assert tdist.auto_mode([5e-3, 5e-3, 1e-3, 1e-3, 1e-3]) == "lpt"
+
+
+def test_warm_up_leaves_no_state():
+    from paper_1909_10616_b200 import tiletune as tt
+    sp = tt.make_space(4096, 4096, 4096, family=tt.FAM_BF16_UMMA)
+    ev = tdist.ShardedEvaluator(lambda s: 1.0, space=sp)
+    ev.warm_up(tt.enumerate_configs(sp, 0, 16))
+    assert ev.known == {} and ev._known_code == {} and ev._over == 0.0 and ev._over_obs == []
+    assert ev.rounds == 0 and ev.plan_s == 0.0

@@ -22,7 +22,7 @@ def main():
     Mr, N, K, fam, budget = bench.WORKLOADS[wl]
     if len(sys.argv) > 2:
         budget = int(sys.argv[2])
-    args = argparse.Namespace(seed=0, width=16, tune_l2_flush=True, assign="lpt", dump_tuning=None)
+    args = argparse.Namespace(seed=0, width=16, tune_l2_flush=True, assign="lpt", dump_tuning=None, two_phase=True)
     ctx = tt.Context(0, input_seed=1)
     sp = tt.make_space(Mr, N, K, family=fam)
     bench.tune(ctx, sp, Mr, N, K, fam, tt.LAYOUT_NN, 8, args, 1, None, 0)        # warm the module
@@ -32,7 +32,8 @@ def main():
     best, rec = bench.tune(ctx, sp, Mr, N, K, fam, tt.LAYOUT_NN, budget, args, 1, None, 0)
     pr.disable()
     print("wall", time.perf_counter() - t0, "tuning_wall", rec["tuning_wall_s"], "proj8",
-          rec["projected_sharded_search"]["by_gpus"]["8"], "host", rec["projected_sharded_search"]["host_s"])
+          rec["projected_sharded_search"]["by_gpus"]["8"], "host", rec["projected_sharded_search"]["host_s"],
+          "plan", rec["projected_sharded_search"]["plan_s_1gpu"])
     pstats.Stats(pr).sort_stats("tottime").print_stats(25)
 
 
