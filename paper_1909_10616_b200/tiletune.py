@@ -163,11 +163,10 @@ def make_space(M: int, N: int, K: int, dm: int = 4, dk: int = 2, dn: int = 4, fa
 
 
 def to_config(s: State) -> Config:
-    c = Config()
-    for a, arr in enumerate((c.m, c.k, c.n)):
-        for i in range(MAXD):
-            arr[i] = s[a][i] if i < len(s[a]) else 1
-    return c
+    """tt_config of a state (unused inner slots = 1).  A fresh object every call (callers may
+    keep it), built from padded tuples in one constructor call: searches marshal every candidate."""
+    pad = (1,) * MAXD
+    return Config((tuple(s[0]) + pad)[:MAXD], (tuple(s[1]) + pad)[:MAXD], (tuple(s[2]) + pad)[:MAXD])
 
 
 def from_config(c: Config, depths=(4, 2, 4)) -> State:
