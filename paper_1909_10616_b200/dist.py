@@ -133,9 +133,12 @@ class ShardedEvaluator:
         self.plan_s = 0.0                        # host seconds spent planning rounds (replicated work)
         self._over = 0.0                         # calibrated per-launch overhead (weights)
         self._over_obs: List[float] = []
+        self._over1 = 0.0                        # calibrated overhead of a phase-1 probe call
+        self._over1_obs: List[float] = []
         self._nb_cache: dict = {}
         self.speculate = speculate
         self.cache: dict = {}                # speculative costs not yet requested by the search
+        self.probe_cache: dict = {}          # speculative cold probes (phase 1) not yet requested
         self.spec_measured = 0
         self.spec_used = 0
         self.round_states: List[list] = []
@@ -325,7 +328,8 @@ class ShardedEvaluator:
 
         Round 0 (s0 alone, fewer candidates than ranks): the idle ranks measure g(s0) (Eq. 9
         under reading Z4), from which round 1 of G-BFS draws all of its candidates (Alg. 1 line
-        6) -- every state, spread over the idle ranks.
+        6) -- every state, spread over the idle ranks; with a phase measurer only their cold
+        probes (``_measure_spec``), and round 1 finishes the ones it draws.
         (Speculating later rounds -- the unmeasured neighbours of the states the next G-BFS round
         is expected to pop, filling each rank's idle time -- was simulated on the measured bf16
         4096^3 costs, tools/spec_study.py: with W = 16 the ranks' idle time rarely fits a whole
@@ -337,7 +341,7 @@ class ShardedEvaluator:
         if self.rounds == 0:
             if self.world <= len(sub):
                 return [], []
-            seen = set(sub) | set(self.known) | set(self.cache)
+            seen = set(sub) | set(self.known) | set(self.cache) | set(self.probe_cache)
             out = []
             for s in sub:
                 for t in self._neighbors(s):
@@ -362,11 +366,18 @@ class ShardedEvaluator:
         preds = self._predicted_costs(sub) if self.assign in ("lpt", "dynamic", "auto") else None
         wts = self.weights(sub, preds) if preds is not None else [1.0] * m
         mode = auto_mode(wts) if self.assign == "auto" else self.assign
-        if self.two_phase(m, mode):
-            # phase 1 = the cold probes, balanced by the predicted probe time (one launch each)
+        cached = [s in self.probe_cache for s in sub]
+        if self.two_phase(m, mode) or (self.measure_phase is not None and any(cached)):
+            # phase 1 = the cold probes, balanced by the predicted probe time (one launch each);
+            # a candidate whose probe was taken speculatively skips it (owner None)
             mode = "two-phase"
-            o = self._over
-            owner = self.lpt_owners([c + o for c in preds], self.world)
+            o = self._over1 if self._over1_obs else self._over
+            idx = [j for j in range(m) if not cached[j]]
+            own = self.lpt_owners([preds[j] + o for j in idx], self.world) if preds is not None else \
+                [q % self.world for q in range(len(idx))]
+            owner = [None] * m
+            for q, j in enumerate(idx):
+                owner[j] = own[q]
             return hit, todo, sub, wts, mode, owner, [], []
         if mode == "dynamic" and self.world > 1:
             owner = None
@@ -401,15 +412,30 @@ class ShardedEvaluator:
         """Run the planning code once on ``states`` with throw-away costs and forget it, so the
         first timed round does not pay Python's and numpy's first-call costs (measured ~3 ms on
         the GPU hosts: more than a whole bf16 round's planning)."""
-        saved = (self.known, self._known_code, self._kc_arrays, self._best, self._over, self._over_obs)
+        saved = (self.known, self._known_code, self._kc_arrays, self._best, self._over, self._over_obs,
+                 self._over1, self._over1_obs)
         self.set_known({s: 1.0 + 1e-3 * i for i, s in enumerate(states)})
         self._over_obs = []
+        self._over1_obs = []
+        self.calibrate_probes([1.0], [1.5])
         self._predicted_costs(list(states))
         self.weights(list(states))
         self.lpt_owners([1.0] * len(states), max(1, self.world))
         self.phase2_plan([1.0] * len(states), [False] * len(states), 0.0)
         self._calibrate([1.0], [2.0], 1.0, 0.0)
-        (self.known, self._known_code, self._kc_arrays, self._best, self._over, self._over_obs) = saved
+        (self.known, self._known_code, self._kc_arrays, self._best, self._over, self._over_obs,
+         self._over1, self._over1_obs) = saved
+
+    def _measure_spec(self, spec, mine):
+        """(values, final flags, seconds) of the speculative states this rank owns.  With a phase
+        measurer only their cold probes: in round 0 there is no incumbent yet, so racing could not
+        shorten whole measurements (a 0.4 ms bf16 config would run all 11 launches); the round
+        that requests a state finishes it with the incumbent known (phase 2).  A probe the slow
+        cut decides is final.  Without a phase measurer: whole measurements."""
+        if self.measure_phase is not None:
+            return self.measure_phase(spec, mine, 1, None)
+        c, t = self.measure_set(spec, mine)
+        return c, [True] * len(spec), t
 
     def _exchange(self, vals):
         """all_reduce(MAX) of a host float vector whose entries only the owning rank filled."""
@@ -428,15 +454,20 @@ class ShardedEvaluator:
         m = len(sub)
         mine = [o == self.rank for o in owner]
         v1 = [0.0] * (3 * m)                   # value, final flag, seconds
+        for j, s in enumerate(sub):
+            if owner[j] is None:                 # probed speculatively in an earlier round
+                v1[j] = self.probe_cache.pop(s)
+                self.spec_used += 1
         if any(mine):
             val, fin, sec = self.measure_phase(sub, mine, 1, None)
             for j in range(m):
                 if mine[j]:
                     v1[j], v1[m + j], v1[2 * m + j] = val[j], 1.0 if fin[j] else 0.0, sec[j]
         if self.world > 1:
-            v1 = self._exchange(v1)
+            v1 = self._exchange(v1)           # cached entries are identical on every rank
         probes = v1[:m]
         final = [v1[m + j] > 0.5 for j in range(m)]
+        self.calibrate_probes(probes, v1[2 * m:])
         t0 = time.perf_counter()
         owner2, _ = self.phase2_plan(probes, final, cut)
         self.plan_s += time.perf_counter() - t0
@@ -461,14 +492,28 @@ class ShardedEvaluator:
             vals[m + j] = v1[2 * m + j] + v2[m + j]
         return [(v1[2 * m + j], probes[j], final[j]) for j in range(m)]
 
-    def absorb(self, states, costs, spec, spec_costs, secs=None, cut=0.0):
+    def calibrate_probes(self, probes, secs1):
+        """Phase-1 overhead = median over probed candidates of (seconds - probe): a probe call
+        also pays the candidate's first-launch host setup (plan, tensor maps)."""
+        v = self._over1_obs
+        for p, t in zip(probes, secs1):
+            if p > 0 and t > 0:
+                bisect.insort(v, max(0.0, t - p))
+        if v:
+            self._over1 = v[len(v) // 2]
+
+    def absorb(self, states, costs, spec, spec_costs, secs=None, cut=0.0, spec_final=None):
         """Record a finished round: requested costs become known, their measurement seconds
-        calibrate the weight model, speculative costs wait in the cache until requested."""
+        calibrate the weight model, speculative costs (final) or probes wait in their caches until
+        requested."""
         if secs is not None:
             self._calibrate(costs, secs, self._best, cut)
         for i, t in enumerate(spec):
             if spec_costs[i] > 0:
-                self.cache[t] = spec_costs[i]
+                if spec_final is None or spec_final[i]:
+                    self.cache[t] = spec_costs[i]
+                else:
+                    self.probe_cache[t] = spec_costs[i]
                 self.spec_measured += 1
         for s, c in zip(states, costs):
             self._remember(s, c)
@@ -484,7 +529,8 @@ class ShardedEvaluator:
         m = len(sub)
         self.round_modes.append(mode)
         S = len(spec)
-        vals = [0.0] * (2 * m + 2 * S)          # costs, seconds (this round), then speculative costs, seconds
+        # costs, seconds (this round), then speculative values, seconds, final flags
+        vals = [0.0] * (2 * m + 3 * S)
         p1 = None
         if mode == "two-phase":
             p1 = self._two_phase(sub, owner, cut, vals)
@@ -505,8 +551,8 @@ class ShardedEvaluator:
                     q = int(self.store.add(key + "_spec", 1)) - 1
                     if q >= S:
                         break
-                    c, t = self.measure_set(spec, [i == q for i in range(S)])
-                    vals[2 * m + q], vals[2 * m + S + q] = c[q], t[q]
+                    c, f, t = self._measure_spec(spec, [i == q for i in range(S)])
+                    vals[2 * m + q], vals[2 * m + S + q], vals[2 * m + 2 * S + q] = c[q], t[q], float(f[q])
         else:
             mine = [o == self.rank for o in owner]
             if any(mine):
@@ -517,10 +563,10 @@ class ShardedEvaluator:
                         self.local_evals += 1
             smine = [o == self.rank for o in spec_owner]
             if any(smine):
-                c, t = self.measure_set(spec, smine)
+                c, f, t = self._measure_spec(spec, smine)
                 for i in range(S):
                     if smine[i]:
-                        vals[2 * m + i], vals[2 * m + S + i] = c[i], t[i]
+                        vals[2 * m + i], vals[2 * m + S + i], vals[2 * m + 2 * S + i] = c[i], t[i], float(f[i])
         if self.world > 1 and p1 is None:
             vals = self._exchange(vals)
         if self.world > 1:
@@ -551,7 +597,8 @@ class ShardedEvaluator:
             self.round_phase1.append(tuple(zip(*ph)))
         else:
             self.round_phase1.append(([], [], []))
-        self.absorb(states, costs, spec, vals[2 * m:2 * m + S], secs=secs, cut=cut)
+        self.absorb(states, costs, spec, vals[2 * m:2 * m + S], secs=secs, cut=cut,
+                    spec_final=[v > 0.5 for v in vals[2 * m + 2 * S:2 * m + 3 * S]])
         return costs
 
 
@@ -603,11 +650,12 @@ def simulate_sharded(round_states: Sequence[Sequence], round_costs: Sequence[Seq
     ``per_round_s`` per exchange (two in a two-phase round).  Two-phase rounds split a candidate's
     seconds at its probe: the recorded phase-1 seconds and probe value when the one-GPU run was
     two-phase too (``round_phase1``, ShardedEvaluator.round_phase1), else one launch's share
-    (seconds / launches(cost)) with probe = cost.  A speculative state costs its recorded seconds
-    if the search measured it at some point, else ``spec_time(state)`` (default: the median
-    recorded candidate).  ``cut_of(incumbent)`` gives the slow cut the weights assume
+    (seconds / launches(cost)) with probe = cost.  ``cut_of(incumbent)`` gives the slow cut the weights assume
     (tt.scoring_opts), none if omitted.  Speculation and assignment cannot change the traversal,
-    so the recorded rounds are exactly what the sharded run requests.  Returns {"wall_s",
+    so the recorded rounds are exactly what the sharded run requests.  Round-0 speculation costs
+    each state its probe with ``two_phase`` (recorded phase-1 seconds, else their median), else a
+    whole measurement without an incumbent (11 launches of recorded cost + the calibrated
+    per-launch overhead; ``spec_time(state)`` overrides).  Returns {"wall_s",
     "plan_host_s" (the planning code's own host time), "spec_measured", "spec_used", "modes"}.
     A projection from one-GPU times, not a multi-GPU measurement."""
     ev = ShardedEvaluator(measure_set=lambda st, mi: ([0.0] * len(st), [0.0] * len(st)), space=space,
@@ -618,17 +666,40 @@ def simulate_sharded(round_states: Sequence[Sequence], round_costs: Sequence[Seq
         ev.cut_s = lambda: cut_of(min(ev.known.values())) if ev.known else 0.0
     if assign in ("dynamic", "auto") and world > 1:
         ev.assign = assign
-    rec = {}
-    for rs, rt in zip(round_states, round_times):
-        for s, t in zip(rs, rt):
+    rec, rec_cost, rec_p1 = {}, {}, {}
+    for k, (rs, rt) in enumerate(zip(round_states, round_times)):
+        ph = round_phase1[k] if round_phase1 is not None and k < len(round_phase1) else None
+        for j, (s, t) in enumerate(zip(rs, rt)):
             rec.setdefault(s, t)
+            rec_cost.setdefault(s, round_costs[k][j])
+            if ph is not None and len(ph[0]):
+                rec_p1.setdefault(s, ph[0][j])
     allt = sorted(t for rt in round_times for t in rt)
     med = allt[len(allt) // 2] if allt else 0.0
+    allc = sorted(rec_cost.values())
+    med_c = allc[len(allc) // 2] if allc else 0.0
+    allp = sorted(rec_p1.values())
+    med_p1 = allp[len(allp) // 2] if allp else med / 11
+    # per-launch overhead of the recorded run (the evaluator's calibration rule over every round)
+    est = ShardedEvaluator(measure_set=lambda st, mi: None)
+    if cut_of is not None:
+        est.cut_s = lambda: cut_of(est._best) if math.isfinite(est._best) else 0.0
+    for k, rs in enumerate(round_states):
+        c_ = est.cut_s() if est.cut_s is not None else 0.0
+        est._calibrate(list(round_costs[k]), list(round_times[k]), est._best, c_)
+        for s, c in zip(rs, round_costs[k]):
+            est._remember(s, c)
+    o_est = est._over
 
     def t_of(s):
-        if s in rec:
-            return rec[s]
-        return spec_time(s) if spec_time is not None else med
+        """Seconds of a speculative (round-0) measurement: its cold probe with a phase measurer
+        (the recorded phase-1 seconds, else the median), else the whole measurement, which in
+        round 0 has no incumbent to race against: 11 launches of (cost + overhead)."""
+        if spec_time is not None:
+            return spec_time(s)
+        if two_phase:
+            return rec_p1.get(s, med_p1)
+        return _FULL_LAUNCHES * (rec_cost.get(s, med_c) + o_est)
 
     def lpt_busy(owner, times):
         busy = [0.0] * world
@@ -659,7 +730,12 @@ def simulate_sharded(round_states: Sequence[Sequence], round_costs: Sequence[Seq
                 t1 = [t / n for t, n in zip(times, nl)]
                 probes = cs
                 final = [n == 1 for n in nl]
+            for j, s in enumerate(sub):
+                if owner[j] is None:                        # probe taken speculatively in round 0
+                    ev.probe_cache.pop(s)
+                    ev.spec_used += 1
             t0 = time.perf_counter()
+            ev.calibrate_probes(probes, [0.0 if owner[j] is None else t1[j] for j in range(len(sub))])
             owner2, _ = ev.phase2_plan(probes, final, cut)
             host += time.perf_counter() - t0
             t2 = [t - a for t, a in zip(times, t1)]
@@ -684,7 +760,8 @@ def simulate_sharded(round_states: Sequence[Sequence], round_costs: Sequence[Seq
                 ev.cache.pop(s)
                 ev.spec_used += 1
         ev.absorb(list(states), list(round_costs[k]), spec, [1.0] * len(spec),
-                  secs=[0.0 if hit[j] else round_times[k][j] for j in range(len(states))], cut=cut)
+                  secs=[0.0 if hit[j] else round_times[k][j] for j in range(len(states))], cut=cut,
+                  spec_final=[not two_phase] * len(spec))
     return {"wall_s": wall, "plan_host_s": host, "spec_measured": ev.spec_measured, "spec_used": ev.spec_used,
             "modes": modes}
 
