@@ -36,7 +36,7 @@ def _worker(rank, world, port, algo, out, mode="static"):
         measured.append(s)
         return costs.t2_cost(sp, s)
 
-    if mode == "auto_dyn":                  # auto with every round long enough to claim dynamically
+    if mode.startswith("auto_dyn"):         # auto with every round long enough to claim dynamically
         tdist._AUTO_CLAIMS = 0
     amode = "auto" if mode.startswith("auto") else ("lpt" if mode == "two_phase" else mode)
     phase_log = []
@@ -64,7 +64,7 @@ def _worker(rank, world, port, algo, out, mode="static"):
         return tdist.ShardedEvaluator(measure_one, store=tdist.default_store() if amode in ("dynamic", "auto") else None,
                                       assign=amode if amode != "dynamic" else None,
                                       space=tt.make_space(64, 64, 64) if amode in ("lpt", "auto") else None,
-                                      measure_phase=measure_phase if mode == "two_phase" else None)
+                                      measure_phase=measure_phase if mode.endswith("two_phase") else None)
 
     ev = make()
     assert ev.assign == amode
@@ -88,7 +88,7 @@ def _worker(rank, world, port, algo, out, mode="static"):
 @pytest.mark.parametrize("algo,mode", [("gbfs", "static"), ("na2c", "static"), ("gbfs", "dynamic"),
                                        ("na2c", "dynamic"), ("gbfs", "lpt"), ("na2c", "lpt"),
                                        ("gbfs", "auto"), ("gbfs", "auto_dyn"), ("gbfs", "two_phase"),
-                                       ("na2c", "two_phase")])
+                                       ("na2c", "two_phase"), ("gbfs", "auto_dyn_two_phase")])
 def test_sharded_search_matches_oracle(algo, mode):
     world = 2
     mgr = mp.Manager()
@@ -106,7 +106,11 @@ def test_sharded_search_matches_oracle(algo, mode):
     assert md0 == md1                                      # every rank took the same per-round modes
     if mode == "auto_dyn":
         assert md0 == ["dynamic"]
-    if mode == "two_phase":
+    if mode == "auto_dyn_two_phase":
+        # dynamic claims everywhere (speculative probes of g(s0) claimed in round 0), except the
+        # round that finishes those probes, which runs its phase 2 as a two-phase round
+        assert md0 == ["dynamic", "two-phase"]
+    if mode.endswith("two_phase"):
         # rounds with more candidates than ranks (or with probes taken speculatively in round 0)
         # ran in two phases; over both ranks every state was probed at most once, every requested
         # state was completed exactly once (whole, by its probe when the probe decided it -- cost
@@ -125,11 +129,11 @@ def test_sharded_search_matches_oracle(algo, mode):
         assert set(done) - set(requested) <= {s for s in g0 if costs.t2_cost(sp64, s) > 1.8}
     assert t0 == t1 == ref                                 # identical traversal on every rank = oracle
     assert sp0 == sp1                                      # every rank agrees on the speculation
-    if mode in ("lpt", "auto", "auto_dyn", "two_phase"):   # g(s0) measured while s0 runs (1 idle rank)
+    if mode != "static" and mode != "dynamic":             # g(s0) measured while s0 runs (1 idle rank)
         assert sp0[0] == len(space.neighbors(sp, space.initial_state(sp))) and 5 <= sp0[1] <= sp0[0]
     else:
         assert sp0 == (0, 0, 0, 0)
-    if mode != "two_phase":
+    if not mode.endswith("two_phase"):
         assert n0 + n1 == len(ref) + sp0[0] - sp0[1]       # each candidate measured exactly once
     if mode == "static":
         assert abs(n0 - n1) <= rounds0                     # round-robin balance
@@ -137,7 +141,7 @@ def test_sharded_search_matches_oracle(algo, mode):
     # second search in the same group: still the oracle traversal, each candidate measured once
     o2 = ogbfs.gbfs(sp, ogbfs.table_source(sp, tab), budget=120, rho=5, seed=9, width=4)
     assert u0 == u1 == [(r.state, r.cost) for r in o2.trace]
-    if mode != "two_phase":
+    if not mode.endswith("two_phase"):
         assert m0 + m1 == 120 + sp0[2] - sp0[3]
 
 
