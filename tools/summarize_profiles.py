@@ -103,11 +103,19 @@ def main():
                   "ends is not counted by the kernel's DRAM counters."]
     with open(os.path.join(PROF, f"{tag}_ncu_k_umma.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
-    merge_traffic(tag, workload, [cfg["m"], cfg["k"], cfg["n"]])
+    clk = m.get("sm__cycles_elapsed.avg.per_second")
+    ten = m.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed")
+    extra = {}
+    if clk:
+        g = float(clk[0].replace(",", "")) * {"Ghz": 1.0, "Mhz": 1e-3, "hz": 1e-9}.get(clk[1], 1.0)
+        extra = {"sm_clock_ghz_ncu": g, "tensor_active_pct_ncu": float(ten[0]) if ten else None,
+                 "clock_source": f"sm__cycles_elapsed.avg.per_second / sm__pipe_tensor_cycles_active of the {tag} "
+                                 f"--set full capture (profiles/{tag}_ncu_k_umma.md)"}
+    merge_traffic(tag, workload, [cfg["m"], cfg["k"], cfg["n"]], extra)
     print("wrote", tag)
 
 
-def merge_traffic(tag, workload, cfg):
+def merge_traffic(tag, workload, cfg, extra=None):
     """Update the bench config's entry of profiles/traffic_<workload>.json (the table bench.py's
     roofline.traffic reads) from gpurun_out/traffic_<tag>.csv (ncu --metrics dram bytes of one
     launch of that config under the current build)."""
@@ -125,7 +133,8 @@ def merge_traffic(tag, workload, cfg):
     entry = {"config": cfg, "dram_bytes_per_launch": vals.get("dram__bytes_read.sum", 0) + vals.get("dram__bytes_write.sum", 0),
              "dram_read": vals.get("dram__bytes_read.sum"), "dram_write": vals.get("dram__bytes_write.sum"),
              "lts_bytes": vals.get("lts__t_bytes.sum"), "ncu_duration_ns": vals.get("gpu__time_duration.sum"),
-             "captured": f"{tag} (tools/gpu_r11_final.sh, current split policy)"}
+             "captured": f"{tag} (tools/gpu_{tag}_final.sh, current split policy)"}
+    entry.update(extra or {})
     tp = os.path.join(PROF, f"traffic_{workload}.json")
     table = json.load(open(tp)) if os.path.exists(tp) else {"workload": workload, "configs": []}
     table.setdefault("configs", [])
