@@ -409,14 +409,13 @@ def traffic_of(workload, best):
     return traffic_entry(workload, best).get("dram_bytes_per_launch")
 
 
-def fp32_record(ctx, args, world, coll, local, dev, peaks, peak_src, sm_max):
+def fp32_record(ctx, args, world, coll, local, dev, peaks, peak_src, sm_max, name):
     """The paper's own arithmetic (fp32 CUDA-core FFMA, reading Z13) on its square workload: G-BFS
     at 0.1 % of the raw space from the untiled s0, then timed steps of the best
     config, as a fraction of the FFMA peak."""
     import torch
 
     from paper_1909_10616_b200 import tiletune as tt
-    name = args.fp32_workload
     Mr, N, K, fam, budget = WORKLOADS[name]
     sp = tt.make_space(Mr, N, K, family=fam)
     best, rec = tune(ctx, sp, Mr, N, K, fam, tt.LAYOUT_NN, budget, args, world, coll, local)
@@ -460,8 +459,9 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=16)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--fp32-workload", default="f32_2048", choices=[k for k in WORKLOADS if k.startswith("f32")],
-                    help="workload of the fp32 (paper arithmetic) record")
+    ap.add_argument("--fp32-workload", default="f32_2048,f32_4096",
+                    help="comma-separated workloads of the fp32 (paper arithmetic) records: the first is 'fp32', "
+                         "the rest 'fp32_more' (f32_2048 = BASELINE config 3; f32_4096 = the bf16 headline's shape)")
     ap.add_argument("--no-fp32", action="store_true", help="skip the fp32 record")
     ap.add_argument("--config", default=None, help="skip tuning and use this config (JSON triple)")
     ap.add_argument("--dump-tuning", default=None, help="write per-round / per-candidate tuning data to PATH.*.jsonl")
@@ -569,8 +569,15 @@ def main():
                                "compute": flops_rank / (peak * 1e12) * 1e6}}
     traffic = traffic_of(args.workload, best)
     fp32 = None
+    fp32_more = []
     if not args.no_fp32 and fam != 1:
-        fp32 = fp32_record(ctx, args, world, coll, local, dev, peaks, peak_src, clocks.get("sm_max_mhz"))
+        names = [w for w in args.fp32_workload.split(",") if w]
+        for w in names:
+            if w not in WORKLOADS or not w.startswith("f32"):
+                raise SystemExit(f"--fp32-workload: unknown fp32 workload {w}")
+        recs = [fp32_record(ctx, args, world, coll, local, dev, peaks, peak_src, clocks.get("sm_max_mhz"), w)
+                for w in names]
+        fp32, fp32_more = recs[0], recs[1:]
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, sample = cpu_oracle_sample(Mr, N, K, fam, seconds=args.cpu_seconds)
@@ -597,6 +604,7 @@ def main():
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_note,
                          "algorithmic": f"2*M*N*K = {flops_rank:.4g} flop per launch", "hbm_side": hbm_side},
             "fp32": fp32,
+            "fp32_more": fp32_more,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": "tt_gemm_host (pinned host A,B -> device -> C host)"},
