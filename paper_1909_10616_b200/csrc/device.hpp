@@ -1,6 +1,7 @@
 // Device-side entry points of libtiletune (kernel launchers; no torch types anywhere).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -42,6 +43,9 @@ tt_status simt_prepare(const Space& sp, const State& s, std::string* err);
 // launch of a search pays it.
 tt_status simt_preload(std::string* err);
 tt_status umma_preload(int family, std::string* err);
+// 2-D fp32 tensor map without swizzle (gemm_umma.cu): dims {inner, outer}, box {box_in, box_out}.
+bool encode_map_2d_f32(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_in,
+                       uint32_t box_out, std::string* err);
 tt_status umma_bind(const Space& sp, const State& s, tt_launch_info* info, std::string* err);
 // every cluster's work items (tile, kb0, kb1, order, split) x n of a tcgen05 launch, in walk order
 tt_status umma_schedule(const Space& sp, const State& s, std::vector<std::vector<int32_t>>* per_worker,

@@ -11,15 +11,22 @@
 // tile.  Each output element is one fmaf chain in ascending k (no split-K, no k-interleaved
 // partial sums): the result is bit-identical to the oracle's sequential fmaf reference.
 //
-// B200 mapping: A/B slabs are staged global -> shared with cp.async (LDGSTS), double
-// buffered (2 stages) so the next slab's copy overlaps the FFMA work on the current one; A is
-// transposed on the way in (As[k][m], rows padded by 4 floats so the strided LDGSTS stores are
-// bank-conflict free for BK = 8 warps); register tiles are read with LDS.128 when m3/n3 are
-// multiples of 4 and results are stored with STG.128.
+// B200 mapping: slabs are double buffered (2 stages) so the next slab's copy overlaps the FFMA
+// work on the current one.  B slabs arrive by TMA (one thread issues a 2-D bulk tensor copy of
+// the dense [BK][BN] box per slab, completing on the slot's mbarrier) when the shape allows it,
+// else by cp.async (LDGSTS); A is staged by cp.async and transposed on the way in (As[k][m], rows
+// padded by 4 floats so the strided LDGSTS stores are bank-conflict free for BK = 8 warps);
+// register tiles are read with LDS.128 when m3/n3 are multiples of 4 and results are stored with
+// STG.128.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "device.hpp"
 
@@ -28,6 +35,11 @@ namespace tt {
 namespace {
 
 struct SimtArgs {
+  // B slabs by TMA (b_tma = 1): one thread issues one 2-D bulk tensor copy per slab into a dense
+  // [BK][BN] box and the CTA waits on that slot's mbarrier; the compute warps issue no B copies
+  // (those held 3.7 % / 5.7 % of the time at 2048^3 / 4096^3, profiles/r12_simt_nocopy_ab.txt).
+  CUtensorMap tmB;
+  int b_tma;
   const float* A;
   const float* B;
   float* C;
@@ -113,15 +125,26 @@ __device__ __forceinline__ void fma_frag(const float* a, const float* b, float (
 // tiles otherwise expose the LDS latency).  BKF = 0: the generic instance.
 template <int TM, int TN, int BKF = 0, int LB = max_threads(TM * TN)>
 __global__ void __launch_bounds__(LB)
-k1_simt(SimtArgs p) {
-  extern __shared__ __align__(16) float smem[];
+k1_simt(const __grid_constant__ SimtArgs p) {
+  extern __shared__ __align__(128) float smem[];
   const int BM = p.m1 * p.m2 * TM;
   const int BN = p.n1 * p.n2 * TN;
   const int BK = BKF > 0 ? BKF : p.bk;
-  const int LDA = BM + 4, LDB = BN + 4;
+  const int LDA = BM + 4, LDB = p.b_tma ? BN : BN + 4;   // TMA boxes are dense
   const int NS = p.stages;               // 2 or 3 smem slots (binder: 3 when occupancy allows)
   float* Bs = smem;                      // [NS][BK][LDB]
   float* As = smem + NS * BK * LDB;      // [NS][BK][LDA]
+  // one mbarrier per slot for the TMA-fed B slabs, after the A slots (fits: the dense B rows free
+  // 16 bytes per k-row of every slot, and the binder's smem counts padded rows)
+  const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(As + NS * BK * LDA);
+  if (p.b_tma) {
+    if (threadIdx.x == 0) {
+      for (int s2 = 0; s2 < NS; ++s2)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8u * s2) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
 
   const int T = blockDim.x;
   const int t = threadIdx.x;
@@ -169,10 +192,19 @@ k1_simt(SimtArgs p) {
   const int b_c = (t & (q4 - 1)) << 2, b_r0 = b_fast ? (t >> p.bq_sh) : 0;
 
   auto load = [&](int kt, int buf) {
+#ifdef TT_SIMT_EXP_NOCOPY
+    // experiment build only (tools/ab_simt.sh): no slab copies -- the k-loop runs on whatever the
+    // shared memory holds, to measure what the copy phase costs; results are meaningless
+    return;
+#endif
     float* as = As + buf * BK * LDA;
     float* bs = Bs + buf * BK * LDB;
     const int64_t kb = (int64_t)kt * BK;
     const int na = BM * BK;
+#ifdef TT_SIMT_EXP_NOCOPY_A
+    if (true) {                            // experiment build: no A slab copies
+    } else
+#endif
     if (a_fast) {                          // rows a_r0, a_r0 + a_rstep, ... of column k = kb + a_c
       const float* src = Ab + (int64_t)a_r0 * K + kb + a_c;
       float* dst = as + a_c * LDA + a_r0;
@@ -207,7 +239,21 @@ k1_simt(SimtArgs p) {
         cp_async4(as + c * LDA + r, Ab + (int64_t)r * K + kb + c);
       }
     }
-    if (b_fast) {                          // rows b_r0, b_r0 + b_rstep, ... of 16-byte column b_c
+#ifdef TT_SIMT_EXP_NOCOPY_B
+    return;
+#endif
+    if (p.b_tma) {                         // one thread: arm the slot's barrier, issue the box
+      if (threadIdx.x == 0) {
+        const uint32_t bar = bar0 + 8u * (uint32_t)buf;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // slot reads done (barrier) -> async writes
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"((uint32_t)(BK * BN * 4)) : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+            ::"r"((uint32_t)__cvta_generic_to_shared(bs)), "l"(&p.tmB), "r"((int)(blockIdx.x * BN)), "r"((int)kb),
+            "r"(bar) : "memory");
+      }
+    } else if (b_fast) {                          // rows b_r0, b_r0 + b_rstep, ... of 16-byte column b_c
       const float* src = Bb + (kb + b_r0) * N + b_c;
       float* dst = bs + b_r0 * LDB + b_c;
       const int64_t sstep = (int64_t)b_rstep * N;
@@ -270,7 +316,16 @@ k1_simt(SimtArgs p) {
     cp_async_commit();
     if (NS == 3) cp_async_wait<2>();
     else cp_async_wait<1>();
+    if (p.b_tma) {                         // slot buf's B box landed (its (kt / NS)-th fill)
+      const uint32_t bar = bar0 + 8u * (uint32_t)buf, par = (uint32_t)(kt / NS) & 1u;
+      uint32_t ok = 0;
+      while (!ok)
+        asm volatile("{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+                     "selp.b32 %0, 1, 0, P;\n\t}" : "=r"(ok) : "r"(bar), "r"(par) : "memory");
+    }
+#ifndef TT_SIMT_EXP_NOSYNC
     __syncthreads();
+#endif
     const float* as = As + buf * BK * LDA + row0;
     const float* bs = Bs + buf * BK * LDB + col0;
     // fragments for step kk+1 are loaded from shared memory while step kk's FMAs issue
@@ -286,7 +341,9 @@ k1_simt(SimtArgs p) {
     }
     if (kk < BK) fma_frag<TM, TN, kPair>(a0, b0, acc, acc2);   // odd BK: last step
     if (++buf == NS) buf = 0;
+#ifndef TT_SIMT_EXP_NOSYNC
     __syncthreads();
+#endif
   }
   if constexpr (kPair) {
 #pragma unroll
@@ -318,7 +375,7 @@ k1_simt(SimtArgs p) {
   }
 }
 
-using KernelFn = void (*)(SimtArgs);
+using KernelFn = void (*)(const SimtArgs);
 
 template <int LM, int LN>
 constexpr KernelFn kfn() {
@@ -468,6 +525,35 @@ tt_status simt_prepare(const Space& sp, const State& s, std::string* err) {
   return pick_instance(sp, s, &pk, err);
 }
 
+namespace {
+// TT_SIMT_TMA=0 (A/B experiments) keeps the cp.async B copies; read at every launch
+bool simt_tma_enabled() {
+  const char* e = std::getenv("TT_SIMT_TMA");
+  return !(e && e[0] == '0');
+}
+
+// Tensor map of B's slabs, cached per (device, pointer, N, K, box): a measurement replays the same
+// launch many times and a search keeps its operands, so the encode runs once per config.
+tt_status simt_b_map(const float* B, int64_t N, int64_t K, uint32_t bn, uint32_t bk, CUtensorMap* out,
+                     std::string* err) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, const float*, int64_t, int64_t, uint32_t, uint32_t>, CUtensorMap> cache;
+  int dev = 0;
+  if (!cuda_ok(cudaGetDevice(&dev), err, "cudaGetDevice")) return TT_E_CUDA;
+  const auto key = std::make_tuple(dev, B, N, K, bn, bk);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return TT_OK;
+  }
+  if (!encode_map_2d_f32(out, B, (uint64_t)N, (uint64_t)K, bn, bk, err)) return TT_E_CUDA;
+  if (cache.size() >= 4096) cache.clear();
+  cache[key] = *out;
+  return TT_OK;
+}
+}  // namespace
+
 tt_status simt_launch(const Space& sp, const State& s, const float* A, const float* B, float* C,
                       cudaStream_t stream, std::string* err, int64_t max_rows) {
   Pick pk;
@@ -476,6 +562,7 @@ tt_status simt_launch(const Space& sp, const State& s, const float* A, const flo
   const tt_launch_info& li = pk.li;
   KernelFn fn = pk.fn;
   SimtArgs a;
+  std::memset(&a, 0, sizeof(a));
   a.A = A;
   a.B = B;
   a.C = C;
@@ -497,8 +584,16 @@ tt_status simt_launch(const Space& sp, const State& s, const float* A, const flo
   a.a_tn = sp.layout == TT_LAYOUT_TN ? 1 : 0;
   a.c_vec = (a.N % 4 == 0 && ((uintptr_t)C % 16) == 0) ? 1 : 0;
   a.stages = li.stages;
+  a.b_tma = 0;
+  if (simt_tma_enabled() && a.b_vec && li.tile_n <= 256 && a.bk >= 8 && a.bk <= 256 &&
+      ((int64_t)a.bk * li.tile_n * 4) % 128 == 0) {
+    tt_status st = simt_b_map(B, a.N, a.K, (uint32_t)li.tile_n, (uint32_t)a.bk, &a.tmB, err);
+    if (st != TT_OK) return st;
+    a.b_tma = 1;
+  }
+  const int64_t ldb = a.b_tma ? li.tile_n : li.tile_n + 4;
   a.a_vec16 = (li.tile_m % 4 == 0 && a.M % 4 == 0 && ((uintptr_t)A % 16) == 0 &&
-               ((2 * (int64_t)a.bk * (li.tile_n + 4)) % 4) == 0) ? 1 : 0;
+               ((2 * (int64_t)a.bk * ldb) % 4) == 0) ? 1 : 0;
   // max_rows > 0 (the partial-grid probe of tt_measure): only the first max_rows CTA rows run
   const int64_t rows = max_rows > 0 ? std::min<int64_t>(max_rows, li.grid_y) : li.grid_y;
   dim3 grid((unsigned)li.grid_x, (unsigned)rows, 1);

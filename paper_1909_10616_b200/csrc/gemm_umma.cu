@@ -779,6 +779,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn(std::string* err) {
 }
 
 CUtensorMapSwizzle swz_enum(int s) {
+  if (s == 0) return CU_TENSOR_MAP_SWIZZLE_NONE;
   if (s == -128) return CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;   // 128B swizzle, 32B atoms (tf32 MN-major)
   return s == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : (s == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
 }
@@ -1220,6 +1221,14 @@ tt_status umma_launch(const Space& sp, const State& s, const void* A, const void
   }
   return pl.cg == 1 ? launch_t<1, 1>(pl, e.ma, e.mb, e.mc, C, stream, err)
                     : launch_t<1, 2>(pl, e.ma, e.mb, e.mc, C, stream, err);
+}
+
+
+// 2-D fp32 tensor map without swizzle (K1's TMA-fed B slabs, gemm_simt.cu): dims {inner, outer},
+// row pitch inner x 4 bytes, box {box_in, box_out}.
+bool encode_map_2d_f32(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_in,
+                       uint32_t box_out, std::string* err) {
+  return make_map(m, 1, ptr, inner, outer, box_in, box_out, 0, err);
 }
 
 }  // namespace tt
