@@ -303,19 +303,36 @@ k1_simt(const __grid_constant__ SimtArgs p) {
     }
   }
 
-  // prologue: slots 0 .. NS-2 in flight; every iteration commits one group (possibly empty) so
-  // wait_group<NS-1> always means "tile kt has landed"
+  // prologue: slots 0 .. NS-2 in flight; every iteration commits one group (possibly empty)
   for (int pk = 0; pk < NS - 1; ++pk) {
     if (pk < p.k0) load(pk, pk);
     cp_async_commit();
   }
   int buf = 0;
+  // one_bar (register tiles of >= 64 accumulators): the copies of slab kt + NS - 1 go out right
+  // after the slab's barrier and a second barrier is not needed; small tiles keep the round-1 loop
+  // (copies issued before the wait, a barrier at the end of the slab), which starts each copy a
+  // little earlier -- that matters when a slab's compute is short (measured as a compile-time
+  // switch: one barrier -1.6 % at 4096^3, -1.1 % at 2048^3, -2 % at 1024^3, +2-5 % for the 8 x 2
+  // tile of 512^3; as a runtime switch inside one instance it bought only 0.5 %, so it is a
+  // compile-time property of the instance; profiles/r12_simt_1bar_ab.txt).
+#ifdef TT_SIMT_TWO_BARRIERS
+  constexpr bool one_bar = false;         // A/B build
+#else
+  constexpr bool one_bar = TM * TN >= 64;
+#endif
   for (int kt = 0; kt < p.k0; ++kt) {
-    const int nxt = kt + NS - 1;
-    if (nxt < p.k0) load(nxt, nxt % NS);
-    cp_async_commit();
-    if (NS == 3) cp_async_wait<2>();
-    else cp_async_wait<1>();
+    if constexpr (!one_bar) {
+      const int nxt = kt + NS - 1;
+      if (nxt < p.k0) load(nxt, nxt % NS);
+      cp_async_commit();
+      if (NS == 3) cp_async_wait<2>();
+      else cp_async_wait<1>();
+    } else {
+      // my copies of slab kt have landed (groups of slabs kt .. kt + NS - 2 were outstanding)
+      if (NS == 3) cp_async_wait<1>();
+      else cp_async_wait<0>();
+    }
     if (p.b_tma) {                         // slot buf's B box landed (its (kt / NS)-th fill)
       const uint32_t bar = bar0 + 8u * (uint32_t)buf, par = (uint32_t)(kt / NS) & 1u;
       uint32_t ok = 0;
@@ -323,9 +340,15 @@ k1_simt(const __grid_constant__ SimtArgs p) {
         asm volatile("{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
                      "selp.b32 %0, 1, 0, P;\n\t}" : "=r"(ok) : "r"(bar), "r"(par) : "memory");
     }
-#ifndef TT_SIMT_EXP_NOSYNC
+    // Slab kt is now visible to every thread.  With one_bar every thread has also finished
+    // computing on slab kt - 1, whose slot ((kt - 1) mod NS = (kt + NS - 1) mod NS) the copies of
+    // slab kt + NS - 1 issued right after this barrier overwrite.
     __syncthreads();
-#endif
+    if constexpr (one_bar) {
+      const int nxt = kt + NS - 1;
+      if (nxt < p.k0) load(nxt, nxt % NS);
+      cp_async_commit();
+    }
     const float* as = As + buf * BK * LDA + row0;
     const float* bs = Bs + buf * BK * LDB + col0;
     // fragments for step kk+1 are loaded from shared memory while step kk's FMAs issue
@@ -341,9 +364,7 @@ k1_simt(const __grid_constant__ SimtArgs p) {
     }
     if (kk < BK) fma_frag<TM, TN, kPair>(a0, b0, acc, acc2);   // odd BK: last step
     if (++buf == NS) buf = 0;
-#ifndef TT_SIMT_EXP_NOSYNC
-    __syncthreads();
-#endif
+    if constexpr (!one_bar) __syncthreads();
   }
   if constexpr (kPair) {
 #pragma unroll
