@@ -226,7 +226,20 @@ def run_reference(args):
     }))
 
 
-def tune(ctx, sp, Mr, N, K, fam, layout, budget, args, world, coll, local):
+# G-BFS width W per workload when --width is not given (reading Z9; the same for every GPU count).
+# W = 16 gives a sharded round enough candidates and finds the same configs as W = 1 at the
+# tensor-core spaces and fp32 2048^3 / 4096^3; at the 0.1 % budgets of 512^3 (484 evaluations) and
+# 1024^3 (900) a round of 16 pops spends the budget breadth-first and stalls far from the optimum:
+# f32_1024 19-23 TF/s at W = 16 vs 32.7-33.0 at W = 1 / 4, f32_512 4-5.5 vs 14.1-14.4 at W = 1
+# (3 seeds each, profiles/r13_width_small_fp32.txt).
+DEFAULT_WIDTH = {"f32_512": 1, "f32_1024": 4}
+
+
+def width_of(args, workload):
+    return args.width if args.width is not None else DEFAULT_WIDTH.get(workload, 16)
+
+
+def tune(ctx, sp, Mr, N, K, fam, layout, budget, args, world, coll, local, workload):
     """G-BFS over the config space with candidate rounds sharded over the ranks (SURVEY §8e);
     candidates are scored under the timed region's protocol (L2 flushed before every timed
     launch) so the search optimises what the bench reports.  Returns (best, tuning record)."""
@@ -235,7 +248,8 @@ def tune(ctx, sp, Mr, N, K, fam, layout, budget, args, world, coll, local):
     import torch.distributed as dist
 
     raw, feasible = tt.count_configs(sp, feasible=True)
-    sopts = tt.search_opts(family=fam, seed=args.seed, width=args.width, layout=layout,
+    width = width_of(args, workload)
+    sopts = tt.search_opts(family=fam, seed=args.seed, width=width, layout=layout,
                            measure={"l2_flush": 1 if args.tune_l2_flush else 0})
     ms_fn, observe, cut_fn, mp_fn = tdist.device_measure_set(ctx, sp, sopts, device=local)
     store = tdist.default_store() if (world > 1 and args.assign in ("dynamic", "auto")) else None
@@ -249,7 +263,7 @@ def tune(ctx, sp, Mr, N, K, fam, layout, budget, args, world, coll, local):
     t0 = time.perf_counter()
     res = tt.gbfs_search(Mr, N, K, budget, sopts, batch=ev)
     tune_wall = tdist.max_over_ranks(time.perf_counter() - t0, coll)
-    rec = {"algorithm": "G-BFS (Alg. 1, width %d, rho 5)" % args.width, "budget": budget, "evals": res.evals,
+    rec = {"algorithm": "G-BFS (Alg. 1, width %d, rho 5)" % width, "budget": budget, "evals": res.evals,
            "space_raw": raw, "space_feasible": feasible, "frac_raw": res.frac_raw,
            "frac_feasible": res.frac_feasible, "tuning_wall_s": tune_wall, "best_config": res.best,
            "best_cost_us": res.best_cost * 1e6, "s0_cost_us": res.trace[0]["cost"] * 1e6,
@@ -418,7 +432,7 @@ def fp32_record(ctx, args, world, coll, local, dev, peaks, peak_src, sm_max, nam
     from paper_1909_10616_b200 import tiletune as tt
     Mr, N, K, fam, budget = WORKLOADS[name]
     sp = tt.make_space(Mr, N, K, family=fam)
-    best, rec = tune(ctx, sp, Mr, N, K, fam, tt.LAYOUT_NN, budget, args, world, coll, local)
+    best, rec = tune(ctx, sp, Mr, N, K, fam, tt.LAYOUT_NN, budget, args, world, coll, local, name)
     A = torch.empty(Mr, K, device=dev)
     B = torch.empty(K, N, device=dev)
     C = torch.empty(Mr, N, device=dev)
@@ -446,8 +460,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="bf16_4096", choices=sorted(WORKLOADS))
     ap.add_argument("--budget", type=int, default=None, help="G-BFS evaluation budget (distinct configs)")
-    ap.add_argument("--width", type=int, default=16,
-                    help="G-BFS states popped per round W (reading Z9): the same for every GPU count")
+    ap.add_argument("--width", type=int, default=None,
+                    help="G-BFS states popped per round W (reading Z9): the same for every GPU count; "
+                         "default per workload (DEFAULT_WIDTH, else 16)")
     ap.add_argument("--assign", choices=["auto", "lpt", "static", "dynamic"], default="auto",
                     help="how a round's candidates are spread over the ranks (paper_1909_10616_b200/dist.py)")
     ap.add_argument("--layout", choices=["nn", "tn"], default="nn",
@@ -516,7 +531,7 @@ def main():
         best = tuple(tuple(v) for v in json.loads(args.config))
         tune_rec = None
     else:
-        best, tune_rec = tune(ctx, sp, Mr, N, K, fam, layout, budget, args, world, coll, local)
+        best, tune_rec = tune(ctx, sp, Mr, N, K, fam, layout, budget, args, world, coll, local, args.workload)
     info = tt.binding(sp, best)
 
     # ---------------- 2. timed steps of the best-found GEMM on this rank's row shard ----------

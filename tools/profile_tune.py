@@ -25,11 +25,11 @@ def main():
     args = argparse.Namespace(seed=0, width=16, tune_l2_flush=True, assign="lpt", dump_tuning=None, two_phase=True)
     ctx = tt.Context(0, input_seed=1)
     sp = tt.make_space(Mr, N, K, family=fam)
-    bench.tune(ctx, sp, Mr, N, K, fam, tt.LAYOUT_NN, 8, args, 1, None, 0)        # warm the module
+    bench.tune(ctx, sp, Mr, N, K, fam, tt.LAYOUT_NN, 8, args, 1, None, 0, wl)        # warm the module
     pr = cProfile.Profile()
     t0 = time.perf_counter()
     pr.enable()
-    best, rec = bench.tune(ctx, sp, Mr, N, K, fam, tt.LAYOUT_NN, budget, args, 1, None, 0)
+    best, rec = bench.tune(ctx, sp, Mr, N, K, fam, tt.LAYOUT_NN, budget, args, 1, None, 0, wl)
     pr.disable()
     print("wall", time.perf_counter() - t0, "tuning_wall", rec["tuning_wall_s"], "proj8",
           rec["projected_sharded_search"]["by_gpus"]["8"], "host", rec["projected_sharded_search"]["host_s"],
