@@ -318,6 +318,8 @@ k1_simt(const __grid_constant__ SimtArgs p) {
   // compile-time property of the instance; profiles/r12_simt_1bar_ab.txt).
 #ifdef TT_SIMT_TWO_BARRIERS
   constexpr bool one_bar = false;         // A/B build
+#elif defined(TT_SIMT_ONE_BAR_MIN)
+  constexpr bool one_bar = TM * TN >= TT_SIMT_ONE_BAR_MIN;   // A/B build
 #else
   constexpr bool one_bar = TM * TN >= 64;
 #endif
