@@ -65,10 +65,11 @@ class ShardedEvaluator:
     Assignment of a round's candidates to ranks (``assign``):
 
     * ``"lpt"`` (default): longest predicted measurement first, each to the least-loaded rank.
-      The prediction of a candidate is the lowest known cost among its measured neighbours (a
-      neighbour differs by one x2 / /2 move), turned into a measurement time by the
-      scoring rules (one launch above the cut, ~11 below).  Every rank holds the same known
-      costs, so every rank computes the same assignment with no communication.
+      The predicted cost of a candidate is the geometric mean of the known costs of its measured
+      neighbours (a neighbour differs by one x2 / /2 move), turned into seconds by the
+      scoring rules (1 launch above the cut, 3 when racing is expected to stop it, else 11) and
+      the calibrated per-launch overhead.  Every rank holds the same known costs, so every rank
+      computes the same assignment with no communication.
     * ``"static"``: candidate j on rank j mod G.
     * ``"dynamic"`` (``store`` given): ranks claim the next unmeasured candidate, in the LPT
       order of the predictions, from a shared counter (``store.add``) whenever they are free.
@@ -77,15 +78,20 @@ class ShardedEvaluator:
       4096^3, ~1 ms each) do not pay a store round trip apiece, long ones (fp32) balance
       dynamically.
 
-    Speculation (``speculate``, needs ``space``): in round 0 -- s0 alone, so G - 1 ranks would
-    idle -- the idle ranks measure s0's neighbourhood g(s0), from which round 1 draws all of its
-    candidates; their costs are served from a cache when the search asks for them.  Nothing about
-    the traversal changes; ``spec_measured`` / ``spec_used`` count the extra hardware
-    measurements and how many the search consumed.
+    Two-phase rounds (``measure_phase`` given, e.g. from ``device_measure_set``): a round with more
+    candidates than ranks measures every cold probe first (LPT over predicted probe times), then
+    the rest of each unfinished measurement, LPT over predictions made from the exchanged probes.
 
-    Costs are exchanged with one all_reduce(MAX) of an [n] float64 vector whose entries only the
-    measuring rank filled (every cost is > 0), so each candidate is measured exactly once and the
-    costs come back by index.
+    Speculation (``speculate``, needs ``space``): in round 0 -- s0 alone, so G - 1 ranks would
+    idle -- the idle ranks measure s0's neighbourhood g(s0) (only the cold probes when
+    ``measure_phase`` is given), from which round 1 draws all of its candidates; their costs or
+    probes are served from caches when the search asks for them.  Nothing about the traversal
+    changes; ``spec_measured`` / ``spec_used`` count the extra hardware measurements and how many
+    the search consumed.
+
+    Results are exchanged with one all_reduce(MAX) per phase of a float64 vector whose entries
+    only the measuring rank filled (every cost is > 0), so each candidate is measured exactly
+    once and the costs come back by index.
     """
 
     _instances = itertools.count()     # per-process: identical on every rank that builds evaluators in order
@@ -162,7 +168,7 @@ class ShardedEvaluator:
     def _moves(s):
         """Every state one action away from s (Eq. 6: s_x[i] <- 2 s_x[i], s_x[j] <- s_x[j] / 2, s_x[j]
         even), legitimate or not.  Only measured -- hence legitimate -- states are ever looked up in
-        the known costs, so min over these equals min over the legitimate neighbours g(s)."""
+        the known costs, so the known costs among these are those of the measured part of g(s)."""
         for a, f in enumerate(s):
             for i in range(len(f)):
                 for j in range(len(f)):
