@@ -205,6 +205,22 @@ k1_simt(const __grid_constant__ SimtArgs p) {
     if (true) {                            // experiment build: no A slab copies
     } else
 #endif
+#ifdef TT_SIMT_EXP_A16
+    // experiment build only: A rows copied as 16-byte chunks WITHOUT the transpose (results are
+    // wrong), to time what the copy's form costs against the transposing 4-byte copies
+    if (!p.a_tn) {
+      const int q4a = BK >> 2;             // 16-byte chunks per A row of the slab
+      const int rstep = T / q4a;
+      const int c = (t % q4a) << 2;
+      const float* src = Ab + (int64_t)(t / q4a) * K + kb + c;
+      float* dst = as + (t / q4a) * BK + c;
+      for (int r = t / q4a; r < BM; r += rstep) {
+        cp_async16(dst, src);
+        dst += rstep * BK;
+        src += (int64_t)rstep * K;
+      }
+    } else
+#endif
     if (a_fast) {                          // rows a_r0, a_r0 + a_rstep, ... of column k = kb + a_c
       const float* src = Ab + (int64_t)a_r0 * K + kb + a_c;
       float* dst = as + a_c * LDA + a_r0;
