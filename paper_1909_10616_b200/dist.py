@@ -624,10 +624,13 @@ def device_measure_set(ctx: tt.Context, sp: tt.Space, opts: tt.SearchOpts, devic
     Returns (measure_set, observe, cut_s, measure_phase) where observe(costs) updates the
     incumbent, cut_s() is the current cut (for the weights) and measure_phase(states, mine, phase,
     probes) is the two-phase form (tt_measure_phase)."""
-    state = {"best": math.inf}
+    state = {"best": math.inf, "mo": None, "mo_best": None}
 
-    def mo():
-        return tt.scoring_opts(sp, opts, state["best"], device)
+    def mo():                                # one tt_scoring_opts call per incumbent value
+        if state["mo_best"] != state["best"]:
+            state["mo"] = tt.scoring_opts(sp, opts, state["best"], device)
+            state["mo_best"] = state["best"]
+        return state["mo"]
 
     def measure_set(states, mine):
         return ctx.measure_set(sp, states, mine, mo())

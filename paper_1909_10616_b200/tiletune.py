@@ -471,7 +471,11 @@ def search_opts(**kw) -> SearchOpts:
 
 
 class SearchResult:
-    def __init__(self, res: Result, trace: List[dict], depths):
+    """A search's result.  ``trace`` (one dict per evaluated state, in evaluation order) is built
+    from the library's tt_trace_row array on first access: a sharded search runs on every rank,
+    and the conversion is presentation, not search work."""
+
+    def __init__(self, res: Result, rows, n: int, depths):
         self.best = from_config(res.best, depths)
         self.best_cost = res.best_cost_s
         self.evals = res.evals
@@ -480,7 +484,17 @@ class SearchResult:
         self.frac_raw = res.frac_raw
         self.frac_feasible = res.frac_feasible
         self.wall_s = res.wall_s
-        self.trace = trace
+        self._rows, self._n, self._depths = rows, n, depths
+        self._trace = None
+
+    @property
+    def trace(self) -> List[dict]:
+        if self._trace is None:
+            r, d = self._rows, self._depths
+            self._trace = [dict(eval_index=r[i].eval_index, t_wall_s=r[i].t_wall_s, state=from_config(r[i].cfg, d),
+                                cost=r[i].cost_s, best=r[i].best_so_far_s) for i in range(self._n)]
+            self._rows = None
+        return self._trace
 
 
 def _search(fn, name, M, N, K, budget, opts: SearchOpts, ctx: Optional[Context], cost=None, table=None,
@@ -521,9 +535,7 @@ def _search(fn, name, M, N, K, budget, opts: SearchOpts, ctx: Optional[Context],
     st = fn(ctx.h if ctx else None, M, N, K, budget, C.byref(opts), C.byref(res), trace, cap)
     _check(st, name)
     d = (opts.dm, opts.dk, opts.dn)
-    rows = [dict(eval_index=trace[i].eval_index, t_wall_s=trace[i].t_wall_s, state=from_config(trace[i].cfg, d),
-                 cost=trace[i].cost_s, best=trace[i].best_so_far_s) for i in range(res.trace_len)]
-    return SearchResult(res, rows, d)
+    return SearchResult(res, trace, res.trace_len, d)
 
 
 def gbfs_search(M: int, N: int, K: int, budget: int, opts: Optional[SearchOpts] = None,
