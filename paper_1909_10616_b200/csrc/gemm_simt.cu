@@ -354,9 +354,18 @@ k1_simt(const __grid_constant__ SimtArgs p) {
     if (p.b_tma) {                         // slot buf's B box landed (its (kt / NS)-th fill)
       const uint32_t bar = bar0 + 8u * (uint32_t)buf, par = (uint32_t)(kt / NS) & 1u;
       uint32_t ok = 0;
-      while (!ok)
+      uint64_t t0 = 0;
+      while (true) {
         asm volatile("{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
                      "selp.b32 %0, 1, 0, P;\n\t}" : "=r"(ok) : "r"(bar), "r"(par) : "memory");
+        if (ok) break;
+        // watchdog (as in the tcgen05 kernel): a box that never lands traps after 10 s -- a launch
+        // error the host reports -- instead of hanging the GPU
+        uint64_t now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > 10000000000ull) __trap();
+      }
     }
     // Slab kt is now visible to every thread.  With one_bar every thread has also finished
     // computing on slab kt - 1, whose slot ((kt - 1) mod NS = (kt + NS - 1) mod NS) the copies of
