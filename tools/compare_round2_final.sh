@@ -9,4 +9,4 @@ timeout 1800 python -m paper_1909_10616_b200.cli compare --m 1024 --k 1024 --n 1
     --max-evals 900 --seeds 0-9 --repeats 5 --shared-cache --scoring --out $OUT/r13_cmp_f32_1024 > $OUT/r13_cmp_f32_1024.log 2>&1
 timeout 2400 python -m paper_1909_10616_b200.cli compare --m 2048 --k 2048 --n 2048 --family f32 \
     --max-evals 1590 --seeds 0-9 --repeats 5 --shared-cache --scoring --out $OUT/r13_cmp_f32_2048 > $OUT/r13_cmp_f32_2048.log 2>&1
-tail -14 $OUT/r13_cmp_*.log
+tail -n 14 $OUT/r13_cmp_*.log
