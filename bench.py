@@ -439,7 +439,10 @@ def fp32_record(ctx, args, world, coll, local, dev, peaks, peak_src, sm_max, nam
     tt.fill_uniform(A, seed=1)
     tt.fill_uniform(B, seed=2)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    per = time_gemm(tt, A, B, C, fam, best, tt.LAYOUT_NN, max(5, min(args.steps, 20)), 3, flush, world)
+    sampler = ClockSampler(local)             # this record's own clocks: it follows a long tuning pass
+    per = time_gemm(tt, A, B, C, fam, best, tt.LAYOUT_NN, max(5, min(args.steps, 20)), 3, flush, world,
+                    sampler=sampler)
+    clocks = sampler.stop()
     ms = statistics.mean(per)
     flops = 2.0 * Mr * N * K
     achieved = flops / (ms * 1e-3) / 1e12
@@ -449,7 +452,7 @@ def fp32_record(ctx, args, world, coll, local, dev, peaks, peak_src, sm_max, nam
             "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "peak_source": note},
             "tuning": rec, "spot_check_err": spot_check(A, C, Mr, N, K, 0, fam, False),
-            "l2": "flushed (256 MiB memset) before every timed launch"}
+            "clocks": clocks, "l2": "flushed (256 MiB memset) before every timed launch"}
 
 
 def main():
