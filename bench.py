@@ -424,9 +424,11 @@ def traffic_of(workload, best):
 
 
 def fp32_record(ctx, args, world, coll, local, dev, peaks, peak_src, sm_max, name):
-    """The paper's own arithmetic (fp32 CUDA-core FFMA, reading Z13) on its square workload: G-BFS
-    at 0.1 % of the raw space from the untiled s0, then timed steps of the best
-    config, as a fraction of the FFMA peak."""
+    """A secondary record on an fp32-storage workload.  f32_*: the paper's own arithmetic (fp32
+    CUDA-core FFMA, reading Z13) on its square workload, G-BFS at 0.1 % of the raw space from the
+    untiled s0, timed steps of the best config against the FFMA peak.  tf32_*: the
+    TF32 tcgen05 family (BASELINE config 3's TF32 half), G-BFS over its space, against the tf32
+    tensor peak."""
     import torch
 
     from paper_1909_10616_b200 import tiletune as tt
@@ -447,7 +449,7 @@ def fp32_record(ctx, args, world, coll, local, dev, peaks, peak_src, sm_max, nam
     flops = 2.0 * Mr * N * K
     achieved = flops / (ms * 1e-3) / 1e12
     peak, note, bound = peak_of(fam, peaks, peak_src, sm_max)
-    return {"workload": name, "family": "f32_simt", "value": achieved, "unit": "TFLOP/s", "ms_per_step": ms,
+    return {"workload": name, "family": "f32_simt" if fam == 1 else "tf32_umma", "value": achieved, "unit": "TFLOP/s", "ms_per_step": ms,
             "best_config": {"m": list(best[0]), "k": list(best[1]), "n": list(best[2])},
             "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "peak_source": note},
@@ -480,7 +482,9 @@ def main():
     ap.add_argument("--fp32-workload", default="f32_2048,f32_4096",
                     help="comma-separated workloads of the fp32 (paper arithmetic) records: the first is 'fp32', "
                          "the rest 'fp32_more' (f32_2048 = BASELINE config 3; f32_4096 = the bf16 headline's shape)")
-    ap.add_argument("--no-fp32", action="store_true", help="skip the fp32 record")
+    ap.add_argument("--tf32-workload", default="tf32_2048",
+                    help="workload of the TF32 record ('tf32'; BASELINE config 3's TF32 half); empty: none")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the fp32 and tf32 records")
     ap.add_argument("--config", default=None, help="skip tuning and use this config (JSON triple)")
     ap.add_argument("--dump-tuning", default=None, help="write per-round / per-candidate tuning data to PATH.*.jsonl")
     ap.add_argument("--tune-warm", dest="tune_l2_flush", action="store_false",
@@ -596,6 +600,12 @@ def main():
         recs = [fp32_record(ctx, args, world, coll, local, dev, peaks, peak_src, clocks.get("sm_max_mhz"), w)
                 for w in names]
         fp32, fp32_more = recs[0], recs[1:]
+    tf32 = None
+    if not args.no_fp32 and fam != 2 and args.tf32_workload:
+        if args.tf32_workload not in WORKLOADS or not args.tf32_workload.startswith("tf32"):
+            raise SystemExit(f"--tf32-workload: unknown tf32 workload {args.tf32_workload}")
+        tf32 = fp32_record(ctx, args, world, coll, local, dev, peaks, peak_src, clocks.get("sm_max_mhz"),
+                           args.tf32_workload)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, sample = cpu_oracle_sample(Mr, N, K, fam, seconds=args.cpu_seconds)
@@ -623,6 +633,7 @@ def main():
                          "algorithmic": f"2*M*N*K = {flops_rank:.4g} flop per launch", "hbm_side": hbm_side},
             "fp32": fp32,
             "fp32_more": fp32_more,
+            "tf32": tf32,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": "tt_gemm_host (pinned host A,B -> device -> C host)"},
