@@ -555,13 +555,20 @@ def test_umma_best_configs_4096_default_policy(fam, cfg):
         assert info.split_tiles == 256 % 74 + 74          # the headline launches split the last wave + tail
 
 
-def test_simt_best_config_4096_sampled_rows():
-    # K1's reported 4096^3 config (profiles/r7_workloads/bench_f32_4096.json): fmaf-bit-exact rows
-    M = N = K = 4096
-    s = ((64, 2, 2, 16), (128, 32), (16, 16, 2, 8))
+@pytest.mark.parametrize("M,s", [
+    (4096, ((64, 2, 2, 16), (128, 32), (16, 16, 2, 8))),   # profiles/r7_workloads, r13_bench_final.json
+    (4096, ((64, 2, 2, 16), (128, 32), (16, 32, 1, 8))),   # found by the re-entry bench's f32_4096 search
+    (2048, ((16, 4, 2, 16), (32, 64), (8, 8, 4, 8))),      # r13_bench_final.json fp32 (f32_2048)
+    (2048, ((16, 2, 4, 16), (32, 64), (8, 16, 2, 8))),     # found by an r13 f32_2048 search
+    (1024, ((16, 4, 2, 8), (8, 128), (8, 16, 2, 4))),      # r13_workloads f32_1024 (width 4)
+])
+def test_simt_best_config_sampled_rows(M, s):
+    # K1's reported configs at full size, in the launch configuration bench.py times (TMA-fed B
+    # slabs, one barrier per slab for the 128-accumulator tiles): fmaf-bit-exact rows
+    N = K = M
     A, B = host_inputs(M, N, K)
     C = run(tt.FAM_F32_SIMT, s, A, B)
-    rows = np.array([0, 1, 63, 64, 2047, 4000, 4095])
+    rows = np.array([0, 1, 63, 64, M // 2 - 1, M - 96, M - 1])
     assert np.array_equal(C[rows], og.gemm_fmaf(A[rows], B))
     assert og.normwise_error(C[rows], og.gemm_f64_rows(A, B, rows)) <= 1e-4
 
