@@ -483,6 +483,8 @@ def test_conv2d_via_gemm(fam):
 @pytest.mark.parametrize("M,N,K,s", [
     (8192, 8192, 8192, ((16, 2, 2, 128), (128, 64), (32, 1, 1, 256))),     # bench bf16_8192 config
     (1024, 8192, 8192, ((4, 2, 1, 128), (128, 64), (32, 1, 1, 256))),      # C5 shard at 8 GPUs
+    (8192, 8192, 8192, ((16, 2, 2, 128), (128, 64), (32, 1, 2, 128))),     # r13_workloads bf16_8192
+    (1024, 8192, 8192, ((2, 2, 2, 128), (128, 64), (32, 1, 2, 128))),      # r13_workloads shard8
 ])
 def test_bf16_max_sizes_sampled(M, N, K, s):
     # BASELINE configs[4] sizes, in the launch configuration bench.py times; sampled entries
@@ -553,6 +555,24 @@ def test_umma_best_configs_4096_default_policy(fam, cfg):
     assert not np.isnan(C).any()
     if cfg[0] == (16, 2, 1, 128) and cfg[2] == (16, 1, 1, 256):
         assert info.split_tiles == 256 % 74 + 74          # the headline launches split the last wave + tail
+
+
+@pytest.mark.parametrize("fam,cfg", [
+    (3, ((8, 2, 1, 128), (16, 128), (8, 1, 2, 128))),      # r13_workloads bf16_2048
+    (3, ((16, 1, 1, 128), (32, 64), (8, 1, 1, 256))),      # r11_workloads bf16_2048
+    (2, ((8, 2, 1, 128), (32, 64), (8, 1, 2, 128))),       # r13_workloads tf32_2048
+    (2, ((8, 2, 1, 128), (32, 64), (8, 1, 1, 256))),       # r13_bench_final.json tf32 record
+])
+def test_umma_best_configs_2048_default_policy(fam, cfg):
+    # the reported 2048^3 launches (BASELINE config 3's TF32 half, bf16 at the paper's 2048 shape)
+    # under the default split policy, rows crossing any split tiles
+    M = N = K = 2048
+    sp_lib = tt.make_space(M, N, K, family=fam)
+    info, rows = _tail_rows(sp_lib, cfg, M)
+    A, B = host_inputs(M, N, K, bf16=fam == tt.FAM_BF16_UMMA)
+    C = run(fam, cfg, A, B)
+    assert not np.isnan(C).any()
+    assert og.normwise_error(C[rows], og.gemm_f64_rows(A, B, rows)) <= 5e-3, (cfg, info.split_tiles)
 
 
 @pytest.mark.parametrize("M,s", [
