@@ -275,3 +275,26 @@ def test_warm_up_leaves_no_state():
     ev.warm_up(tt.enumerate_configs(sp, 0, 16))
     assert ev.known == {} and ev._known_code == {} and ev._over == 0.0 and ev._over_obs == []
     assert ev.rounds == 0 and ev.plan_s == 0.0
+
+
+def test_projection_two_phase_speculative_probes():
+    # round 0 (s0 alone) on 2 ranks: the idle rank takes only the cold probes of g(s0) (recorded
+    # phase-1 seconds, else their median); round 1 (four of g(s0)) then runs only phase 2
+    from paper_1909_10616_b200 import tiletune as tt
+    sp = tt.make_space(64, 64, 64)
+    s0 = tt.unrank(sp, tt.count_configs(sp) - 1)
+    g = tt.neighbors(sp, s0)
+    rounds = [[s0], g[:4]]
+    rc = [[1e-3], [1e-3, 1e-3, 1e-3, 1e-3]]
+    rt = [[0.011], [0.011, 0.011, 0.011, 0.011]]
+    ph = [([], [], []), ((0.001, 0.002, 0.001, 0.001), (1e-3, 1e-3, 1e-3, 1e-3), (0, 0, 0, 0))]
+    r = tdist.simulate_sharded(rounds, rc, rt, 2, space=sp, two_phase=True, round_phase1=ph, per_round_s=0.0)
+    assert r["modes"][1] == "two-phase" and r["spec_used"] == 4 and r["spec_measured"] == len(g)
+    # round 0: s0 (0.011) vs the probes of g(s0) on the idle rank: 4 recorded (0.005) + the rest at
+    # the recorded median 0.001; round 1: phase 1 free, phase 2 = 4 x 0.010 (or 0.009) over 2 ranks
+    r0 = max(0.011, 0.005 + 0.001 * (len(g) - 4))
+    phase2 = sorted([0.010, 0.009, 0.010, 0.010], reverse=True)
+    load = [0.0, 0.0]
+    for x in phase2:
+        load[load.index(min(load))] += x
+    assert abs(r["wall_s"] - (r0 + max(load))) < 1e-9
