@@ -40,8 +40,12 @@ _RACE_RATIO = 1.1
 # above the final cost), so phase 2 predicts "raced" only beyond it -- predicting a short
 # candidate long costs an LPT plan little, the converse leaves one rank running at the round's end
 _PROBE_MARGIN = 0.1
-# one dynamic claim (a TCPStore add round trip); "auto" claims dynamically only in rounds whose
-# median predicted measurement time is >= _AUTO_CLAIMS claims, else it uses the LPT plan
+# "auto" claims dynamically only in rounds whose median predicted measurement time is >=
+# _AUTO_CLAIMS x _CLAIM_S = 2 ms, else it uses the LPT (or two-phase) plan.  _CLAIM_S is a
+# conservative budget per claim (a TCPStore add round trip plus one measure call's marshalling:
+# 21 us measured on the GPU host, bench.py claim_s); the 2 ms line keeps the bf16 rounds (0.3-2.9
+# ms candidates) on the two-phase plan, which the replays rate above dynamic claiming there
+# (profiles/r12_replay_sharded_bf16_4096.txt), and sends the long fp32 rounds to dynamic claims.
 _CLAIM_S = 200e-6
 _AUTO_CLAIMS = 10
 
